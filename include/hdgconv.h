@@ -1,0 +1,137 @@
+/*
+ * hdgconv.h — C ABI of the B200 (sm_100a) fp64 upwind-DG convection apply.
+ *
+ * Drop-in boundary for the reference's convection entry point
+ *   forms.apply_convection(u_conv, w, data) -> residual over V_h
+ *   (operator PAPER.md:424-436)
+ * and for the explicit substep loop that calls it
+ *   timeloop.propagate_convection,
+ * plus the transfer operators I / I^T.
+ *
+ * Conventions:
+ *  - u_loc (NT, nb): element-local BDM_k coefficients in BDMBasis member
+ *    order: edge e=0..2 x Legendre mode 0..k, then interior moments
+ *    (polybasis.py:265-268, 315-354).
+ *  - w, r (NT, nb): V_h coefficients, index c*nbs + m, c in {x,y}, m in
+ *    dubiner_index(k) order (polybasis.py:174-176, 282-289).
+ *  - inflow (NBF, nf, 2): exterior values on boundary facets, rows in
+ *    boundary-facet order (facet index order of mesh2d.py:178-207), points
+ *    of quad_interval(3k+1) along the owner's traversal.  NULL = interior
+ *    trace everywhere (no inflow data).
+ *  - all fp64, row-major, contiguous.
+ *
+ * Memory: every double* argument of the compute calls is a DEVICE pointer
+ * owned by the caller (no allocation in hot calls), except the *_host
+ * variants, which take pageable or pinned HOST pointers and stage through
+ * context-owned device buffers.  `stream` is a cudaStream_t (NULL = legacy
+ * default stream); all calls are asynchronous on it except the *_host ones,
+ * which synchronise the stream before returning.
+ *
+ * Errors: every call returns 0 on success, a negative HDGC_E* code on
+ * failure; hdgc_last_error() returns a thread-local message.  No C++
+ * exception crosses this boundary.
+ *
+ * Determinism: element-owned passes, no atomics, fixed summation order —
+ * results are bitwise reproducible run to run on the same GPU.
+ */
+#ifndef HDGCONV_H
+#define HDGCONV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HDGC_OK 0
+#define HDGC_EINVAL (-1)   /* bad argument / inconsistent descriptor */
+#define HDGC_ECUDA (-2)    /* CUDA runtime error */
+#define HDGC_ENOMEM (-3)   /* device allocation failed */
+#define HDGC_EUNSUP (-4)   /* unsupported order / dimension */
+
+typedef struct hdgc_ctx hdgc_ctx;
+
+/* Mesh topology + affine geometry, HOST arrays (copied at create).
+ * Mirrors hdgflow.mesh2d.Mesh (mesh2d.py:86-150): CCW triangles, facets in
+ * sorted-vertex-key order, facet_elems[:,1] = -1 on the boundary. */
+typedef struct {
+  int32_t dim;               /* 2 (triangles); 3 (tetrahedra) */
+  int32_t n_vertices;
+  int32_t n_elements;
+  int32_t n_facets;
+  const double* vertices;    /* (NV, dim) */
+  const int64_t* elements;   /* (NT, dim+1) vertex ids */
+  const int64_t* facet_elems;/* (NF, 2) */
+  const int64_t* facet_local;/* (NF, 2) */
+  const int32_t* facet_perm; /* 3D only: (NF,) neighbour face permutation id; NULL in 2D */
+} hdgc_mesh_desc;
+
+/* Reference-element tables, HOST arrays (copied at create), produced by the
+ * host-side basis module (restating polybasis.py:47-378). */
+typedef struct {
+  int32_t k;                 /* polynomial order */
+  int32_t nqv;               /* volume rule size, quad_triangle(3k-1) */
+  int32_t nf;                /* facet rule size, quad_interval(3k+1) (2D) */
+  const double* coef;        /* (nb, nb) BDM dual basis: raw -> member (polybasis.py:357-378) */
+  const double* div_modal;   /* (nbs(k-1), nb) div of each BDM member in the Dubiner P_{k-1} basis */
+  const double* vol_w;       /* (nqv) */
+  const double* vol_D;       /* (nqv, nbs)   Dubiner values */
+  const double* vol_G;       /* (nqv, nbs, dim) Dubiner reference gradients */
+  const double* fac_w;       /* (nf) */
+  const double* fac_L;       /* (nf, nfd) facet normal-trace basis at facet points */
+  const double* fac_D;       /* (nfaces, nf, nbs) Dubiner on each reference facet */
+  const double* fac_len;     /* (nfaces) reference facet measures |e_hat| */
+} hdgc_tables_desc;
+
+typedef struct {
+  int32_t dim, k, nb, nbs, nqv, nf;
+  int32_t n_elements, n_facets, n_boundary_facets;
+  int32_t volume_variant;    /* kernel variant chosen for this k */
+  int64_t device_bytes;      /* context-owned device memory */
+} hdgc_info;
+
+/* Build a context: uploads tables, runs the on-device geometry/adjacency
+ * precompute (Piola factors J/detJ, 2/detJ, neighbour codes, boundary slots). */
+int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tables, hdgc_ctx** out);
+int hdgc_destroy(hdgc_ctx* ctx);
+int hdgc_get_info(const hdgc_ctx* ctx, hdgc_info* info);
+
+/* r = C^V(u; w).  r must not alias u, w or inflow. */
+int hdgc_apply_v(hdgc_ctx* ctx, const double* u_loc, const double* w, const double* inflow,
+                 double* r, void* stream);
+
+/* r_w = I^T C^V(u; I u): the HDG-side operator C^U u, output in
+ * element-local BDM-test layout (same layout as u_loc). */
+int hdgc_apply_w(hdgc_ctx* ctx, const double* u_loc, const double* inflow, double* r_w,
+                 void* stream);
+
+/* nsteps forward-Euler substeps, u frozen, device-resident:
+ *   w <- w - dt * (M^V)^{-1} C^V(u; w),  (M^V)^{-1} = 2/detJ per element. */
+int hdgc_substeps(hdgc_ctx* ctx, const double* u_loc, double* w_inout, const double* inflow,
+                  double dt, int32_t nsteps, void* stream);
+
+/* Transfer operators: direction 0: out = I in (BDM -> V_h),
+ * direction 1: out = I^T in (V_h functionals -> BDM-test layout). */
+int hdgc_transfer(hdgc_ctx* ctx, int32_t direction, const double* in, double* out, void* stream);
+
+/* (M^V)^{-1} diagonal scale per element, out (NT,) = 2/detJ. */
+int hdgc_mass_inverse(hdgc_ctx* ctx, double* out, void* stream);
+
+/* max over elements x volume points of |J u_hat / detJ| into *out_dev (device
+ * double), for the substep size dt = 0.1 h / (k^2 max|u|) (BASELINE cfg2). */
+int hdgc_max_speed(hdgc_ctx* ctx, const double* u_loc, double* out_dev, void* stream);
+
+/* End-to-end variants on HOST buffers: H2D of the inputs, compute, D2H of
+ * the result, all on `stream`, synchronised before return. */
+int hdgc_apply_v_host(hdgc_ctx* ctx, const double* u_loc, const double* w, const double* inflow,
+                      double* r, void* stream);
+int hdgc_substeps_host(hdgc_ctx* ctx, const double* u_loc, double* w_inout, const double* inflow,
+                       double dt, int32_t nsteps, void* stream);
+
+const char* hdgc_last_error(void);
+const char* hdgc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HDGCONV_H */

@@ -1,0 +1,92 @@
+"""ctypes binding of ``libhdgconv.so`` (the C ABI in include/hdgconv.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` /
+``python -m paper_1508_04245_b200.build``.  There is no fallback: if the
+library is missing or fails to load, every operator raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhdgconv.so")
+
+# exported symbols, in include/hdgconv.h order
+SYMBOLS = (
+    "hdgc_create", "hdgc_destroy", "hdgc_get_info", "hdgc_apply_v", "hdgc_apply_w",
+    "hdgc_substeps", "hdgc_transfer", "hdgc_mass_inverse", "hdgc_max_speed",
+    "hdgc_apply_v_host", "hdgc_substeps_host", "hdgc_last_error", "hdgc_version",
+)
+
+_dp = C.POINTER(C.c_double)
+
+
+class MeshDesc(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32), ("n_vertices", C.c_int32), ("n_elements", C.c_int32),
+        ("n_facets", C.c_int32), ("vertices", C.c_void_p), ("elements", C.c_void_p),
+        ("facet_elems", C.c_void_p), ("facet_local", C.c_void_p), ("facet_perm", C.c_void_p),
+    ]
+
+
+class TablesDesc(C.Structure):
+    _fields_ = [
+        ("k", C.c_int32), ("nqv", C.c_int32), ("nf", C.c_int32),
+        ("coef", C.c_void_p), ("div_modal", C.c_void_p), ("vol_w", C.c_void_p), ("vol_D", C.c_void_p),
+        ("vol_G", C.c_void_p), ("fac_w", C.c_void_p), ("fac_L", C.c_void_p),
+        ("fac_D", C.c_void_p), ("fac_len", C.c_void_p),
+    ]
+
+
+class Info(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32), ("k", C.c_int32), ("nb", C.c_int32), ("nbs", C.c_int32),
+        ("nqv", C.c_int32), ("nf", C.c_int32), ("n_elements", C.c_int32),
+        ("n_facets", C.c_int32), ("n_boundary_facets", C.c_int32),
+        ("volume_variant", C.c_int32), ("device_bytes", C.c_int64),
+    ]
+
+
+_LIB = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the library once; raise RuntimeError (no fallback) on failure."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} is missing: build the CUDA extension first "
+            "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+    lib = C.CDLL(path)
+    vp, i32, d = C.c_void_p, C.c_int32, C.c_double
+    sig = {
+        "hdgc_create": ([C.POINTER(MeshDesc), C.POINTER(TablesDesc), C.POINTER(vp)], C.c_int),
+        "hdgc_destroy": ([vp], C.c_int),
+        "hdgc_get_info": ([vp, C.POINTER(Info)], C.c_int),
+        "hdgc_apply_v": ([vp, vp, vp, vp, vp, vp], C.c_int),
+        "hdgc_apply_w": ([vp, vp, vp, vp, vp], C.c_int),
+        "hdgc_substeps": ([vp, vp, vp, vp, d, i32, vp], C.c_int),
+        "hdgc_transfer": ([vp, i32, vp, vp, vp], C.c_int),
+        "hdgc_mass_inverse": ([vp, vp, vp], C.c_int),
+        "hdgc_max_speed": ([vp, vp, vp, vp], C.c_int),
+        "hdgc_apply_v_host": ([vp, vp, vp, vp, vp, vp], C.c_int),
+        "hdgc_substeps_host": ([vp, vp, vp, vp, d, i32, vp], C.c_int),
+        "hdgc_last_error": ([], C.c_char_p),
+        "hdgc_version": ([], C.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _LIB = lib
+    return lib
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        msg = load().hdgc_last_error().decode(errors="replace")
+        raise RuntimeError(f"{what} failed (status {rc}): {msg}")

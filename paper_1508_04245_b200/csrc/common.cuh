@@ -1,0 +1,65 @@
+// Shared compile-time dimensions and parameter blocks for the 2D
+// convection kernels (sm_100a, fp64).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hdgc {
+
+// Per-order constants.  The volume rule is quad_triangle(3k-1) (exact for the
+// degree 3k-1 volume integrand), the facet rule quad_interval(3k+1) (pinned,
+// SPEC.md:157); see basis.volume_rule / basis.facet_rule.
+template <int K>
+struct Dims {
+  static constexpr int NE = K + 1;                       // Legendre modes per edge
+  static constexpr int NBS = (K + 1) * (K + 2) / 2;      // scalar P_k
+  static constexpr int NB = 2 * NBS;                     // [P_k]^2 = BDM_k
+  static constexpr int NBS1 = K * (K + 1) / 2;           // scalar P_{k-1} (divergence space)
+  static constexpr int NQV = K == 1 ? 3 : (K == 2 ? 7 : ((3 * K + 1) / 2) * ((3 * K + 1) / 2));
+  static constexpr int NF = (3 * K + 3) / 2;
+  // table offsets (doubles) in the packed device table
+  static constexpr int OFF_COEF = 0;
+  static constexpr int OFF_DIVM = OFF_COEF + NB * NB;
+  static constexpr int OFF_VW = OFF_DIVM + NBS1 * NB;
+  static constexpr int OFF_VD = OFF_VW + NQV;
+  static constexpr int OFF_VG = OFF_VD + NQV * NBS;
+  static constexpr int OFF_FW = OFF_VG + NQV * NBS * 2;
+  static constexpr int OFF_FL = OFF_FW + NF;
+  static constexpr int OFF_FD = OFF_FL + NF * NE;
+  static constexpr int OFF_FLEN = OFF_FD + 3 * NF * NBS;
+  static constexpr int TAB = OFF_FLEN + 4;               // padded to keep 16-B alignment
+};
+
+inline int dims_nqv(int k) {
+  return k == 1 ? 3 : (k == 2 ? 7 : ((3 * k + 1) / 2) * ((3 * k + 1) / 2));
+}
+inline int dims_nf(int k) { return (3 * k + 3) / 2; }
+inline int dims_nbs(int k) { return (k + 1) * (k + 2) / 2; }
+inline int dims_tab(int k) {
+  const int nbs = dims_nbs(k), nb = 2 * nbs, nqv = dims_nqv(k), nf = dims_nf(k);
+  return nb * nb + (k * (k + 1) / 2) * nb + nqv + nqv * nbs + nqv * nbs * 2 + nf + nf * (k + 1) + 3 * nf * nbs + 4;
+}
+
+// Output modes of the element kernel.
+enum : int {
+  MODE_APPLY = 0,    // r = C^V(u; w)
+  MODE_SUBSTEP = 1,  // w_out = w - dt * (2/detJ) * C^V(u; w)
+  MODE_APPLY_IT = 2, // r_w = I^T C^V(u; w)
+};
+
+// Per-element neighbour code: >= 0: (neighbour element << 2) | neighbour local
+// edge; < 0: boundary facet, slot = -1 - code (row of the inflow array).
+struct ElemParams {
+  const double* __restrict__ tab;     // packed reference tables (Dims<K> layout)
+  const double* __restrict__ u;       // (NT, NB) BDM coefficients
+  const double* __restrict__ w;       // (NT, NB) V_h coefficients
+  const double* __restrict__ inflow;  // (NBF, NF, 2) or nullptr
+  const int32_t* __restrict__ code;   // (NT, 3)
+  const double* __restrict__ piola;   // (4, NT) SoA: J/detJ row-major (00, 01, 10, 11)
+  const double* __restrict__ minv;    // (NT,) 2/detJ
+  double* __restrict__ out;           // (NT, NB)
+  double dt;
+  int nt;
+};
+
+}  // namespace hdgc

@@ -1,0 +1,214 @@
+// Variant "thread": one thread per element, fused volume + upwind facets,
+// tables broadcast from shared memory.  Generic in K (1..8); the fallback for
+// orders without a tuned variant.
+//
+// Operator, geometry-free reference form
+// on affine elements, evaluated in the equivalent
+// "flux-difference" form
+//
+//   r[c,m] =  sum_p w_p ( u_hat.grad_hat w_c + w_c div_hat u_hat )(p) D_m(p)
+//           + sum_e sum_{q: F<0} w_q F_e(t_q) ( w_ext - w_own )_c(t_q) D_m(x_e(t_q))
+//
+// which equals the textbook form  -int w (x) u : grad z + int (u.n) w_hat z
+// exactly (divergence theorem; both rules integrate the polynomial integrands
+// exactly: volume degree 3k-1, facet degree 3k), but does not cancel two large
+// terms against each other, so its fp64 rounding error stays ~1e-15 relative
+// where the textbook form loses 2-4 digits on fine meshes.
+//   F_e(t) = |e_hat| sum_l u[e*(k+1)+l] L_l(t)   (= u.n ds/dt)
+//   w_ext  = neighbour trace at t' = 1 - t (mesh2d.py:201), or inflow data
+#pragma once
+#include "common.cuh"
+
+namespace hdgc {
+
+template <int K>
+__host__ __device__ constexpr bool thread_tab_in_smem() { return Dims<K>::TAB * 8 <= 200 * 1024; }
+
+template <int K>
+__host__ __device__ constexpr int thread_smem_bytes() { return thread_tab_in_smem<K>() ? Dims<K>::TAB * 8 : 0; }
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(128)
+conv2d_thread_kernel(ElemParams p) {
+  using D = Dims<K>;
+  constexpr int NB = D::NB, NBS = D::NBS, NBS1 = D::NBS1, NE = D::NE, NF = D::NF, NQV = D::NQV;
+  // tables staged in shared memory when they fit (k <= 7), else read through L1
+  constexpr bool SMEM = thread_tab_in_smem<K>();
+  extern __shared__ __align__(16) double s_tab[];
+  if (SMEM) {
+    for (int i = threadIdx.x; i < D::TAB; i += blockDim.x) s_tab[i] = p.tab[i];
+    __syncthreads();
+  }
+  const double* base = SMEM ? s_tab : p.tab;
+  const double* coef = base + D::OFF_COEF;
+  const double* divm = base + D::OFF_DIVM;
+  const double* vw = base + D::OFF_VW;
+  const double* vD = base + D::OFF_VD;
+  const double* vG = base + D::OFF_VG;
+  const double* fw = base + D::OFF_FW;
+  const double* fL = base + D::OFF_FL;
+  const double* fD = base + D::OFF_FD;
+  const double* flen = base + D::OFF_FLEN;
+
+  const int T = blockIdx.x * blockDim.x + threadIdx.x;
+  if (T >= p.nt) return;
+
+  // modal velocity u_hat = coef u and its modal divergence dv = divm u (in P_{k-1})
+  double uh[NB];
+  double dv[NBS1];
+  {
+    double u[NB];
+    const double* ug = p.u + (size_t)T * NB;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) u[j] = __ldg(ug + j);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      double a = 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) a = fma(coef[i * NB + j], u[j], a);
+      uh[i] = a;
+    }
+#pragma unroll
+    for (int i = 0; i < NBS1; ++i) {
+      double a = 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) a = fma(divm[i * NB + j], u[j], a);
+      dv[i] = a;
+    }
+  }
+  double w[NB];
+  {
+    const double* wg = p.w + (size_t)T * NB;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) w[j] = __ldg(wg + j);
+  }
+  double r[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) r[j] = 0.0;
+
+  // ---- volume: f_c = u.grad w_c + w_c div u, tested against D_m
+#pragma unroll 1
+  for (int q = 0; q < NQV; ++q) {
+    const double* Dq = vD + q * NBS;
+    const double* Gq = vG + q * NBS * 2;
+    double w0 = 0.0, w1 = 0.0, u0 = 0.0, u1 = 0.0, dvq = 0.0;
+    double w0x = 0.0, w0y = 0.0, w1x = 0.0, w1y = 0.0;
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) {
+      const double d = Dq[m], gx = Gq[2 * m], gy = Gq[2 * m + 1];
+      w0 = fma(w[m], d, w0);
+      w1 = fma(w[NBS + m], d, w1);
+      u0 = fma(uh[m], d, u0);
+      u1 = fma(uh[NBS + m], d, u1);
+      w0x = fma(w[m], gx, w0x);
+      w0y = fma(w[m], gy, w0y);
+      w1x = fma(w[NBS + m], gx, w1x);
+      w1y = fma(w[NBS + m], gy, w1y);
+      if (m < NBS1) dvq = fma(dv[m], d, dvq);
+    }
+    const double wt = vw[q];
+    const double f0 = wt * fma(u0, w0x, fma(u1, w0y, w0 * dvq));
+    const double f1 = wt * fma(u0, w1x, fma(u1, w1y, w1 * dvq));
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) {
+      r[m] = fma(f0, Dq[m], r[m]);
+      r[NBS + m] = fma(f1, Dq[m], r[NBS + m]);
+    }
+  }
+
+  // ---- facets: upwind jump on inflow points only (element-owned, no atomics)
+#pragma unroll 1
+  for (int e = 0; e < 3; ++e) {
+    double ue[NE];
+#pragma unroll
+    for (int l = 0; l < NE; ++l) ue[l] = __ldg(p.u + (size_t)T * NB + e * NE + l);
+    const double len = flen[e];
+    double F[NF];
+    bool inflow_edge = false;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      double a = 0.0;
+#pragma unroll
+      for (int l = 0; l < NE; ++l) a = fma(ue[l], fL[q * NE + l], a);
+      F[q] = a * len;
+      inflow_edge |= F[q] < 0.0;
+    }
+    if (!inflow_edge) continue;  // pure outflow edge: w_hat = own trace, jump = 0
+    const int code = __ldg(p.code + (size_t)T * 3 + e);
+    const double* infl = nullptr;
+    double* wn = uh;  // reuse registers: u_hat is dead after the volume term
+    int e2 = 0;
+    if (code >= 0) {
+      const double* wg = p.w + (size_t)(code >> 2) * NB;
+      e2 = code & 3;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) wn[j] = __ldg(wg + j);
+    } else if (p.inflow != nullptr) {
+      infl = p.inflow + (size_t)(-1 - code) * NF * 2;
+    } else {
+      continue;  // boundary without inflow data: exterior value = own trace
+    }
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      const double Fq = F[q];
+      if (!(Fq < 0.0)) continue;
+      const double* De = fD + (e * NF + q) * NBS;
+      double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) {
+        o0 = fma(w[m], De[m], o0);
+        o1 = fma(w[NBS + m], De[m], o1);
+      }
+      double x0, x1;
+      if (code >= 0) {
+        const double* Dn = fD + (e2 * NF + (NF - 1 - q)) * NBS;
+        x0 = 0.0; x1 = 0.0;
+#pragma unroll
+        for (int m = 0; m < NBS; ++m) {
+          x0 = fma(wn[m], Dn[m], x0);
+          x1 = fma(wn[NBS + m], Dn[m], x1);
+        }
+      } else {
+        x0 = __ldg(infl + 2 * q);
+        x1 = __ldg(infl + 2 * q + 1);
+      }
+      const double s = fw[q] * Fq;
+      const double j0 = s * (x0 - o0), j1 = s * (x1 - o1);
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) {
+        r[m] = fma(j0, De[m], r[m]);
+        r[NBS + m] = fma(j1, De[m], r[NBS + m]);
+      }
+    }
+  }
+
+  // ---- epilogue
+  double* og = p.out + (size_t)T * NB;
+  if (MODE == MODE_APPLY) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) og[j] = r[j];
+  } else if (MODE == MODE_SUBSTEP) {
+    const double s = p.dt * __ldg(p.minv + T);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) og[j] = fma(-s, r[j], w[j]);
+  } else {
+    // r_w = I^T r: s[d*nbs+m] = sum_c P[c][d] r[c*nbs+m]; r_w[j] = sum_i coef[i][j] s[i]
+    const double P00 = __ldg(p.piola + T), P01 = __ldg(p.piola + p.nt + T);
+    const double P10 = __ldg(p.piola + 2 * (size_t)p.nt + T), P11 = __ldg(p.piola + 3 * (size_t)p.nt + T);
+    double s[NB];
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) {
+      s[m] = fma(P00, r[m], P10 * r[NBS + m]);
+      s[NBS + m] = fma(P01, r[m], P11 * r[NBS + m]);
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      double a = 0.0;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) a = fma(coef[i * NB + j], s[i], a);
+      og[j] = a;
+    }
+  }
+}
+
+}  // namespace hdgc

@@ -1,0 +1,523 @@
+// hdgconv.cu — C ABI, device context and setup/transfer kernels for the
+// B200 fp64 upwind-DG convection apply.  See include/hdgconv.h.
+#include "../../include/hdgconv.h"
+
+#include <cstdio>
+#include <cstdarg>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "conv2d_thread.cuh"
+
+using namespace hdgc;
+
+// ---------------------------------------------------------------------------
+// error plumbing
+
+static thread_local std::string g_err;
+
+static int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                      \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      return set_err(HDGC_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, \
+                     __LINE__);                                                          \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// context
+
+struct hdgc_ctx {
+  int dim = 2, k = 0, nb = 0, nbs = 0, nqv = 0, nf = 0;
+  int nt = 0, nf_facets = 0, nbf = 0, nv = 0;
+  double* d_tab = nullptr;      // packed tables (Dims<K> layout)
+  int32_t* d_code = nullptr;    // (NT, 3) neighbour codes
+  double* d_piola = nullptr;    // (4, NT) J/detJ
+  double* d_minv = nullptr;     // (NT,) 2/detJ
+  double* d_scratch = nullptr;  // (NT, nb) ping-pong / I u
+  // host-variant staging (lazily allocated)
+  double* d_hu = nullptr;
+  double* d_hw = nullptr;
+  double* d_hr = nullptr;
+  double* d_hin = nullptr;
+  int64_t bytes = 0;
+  int variant = 0;
+};
+
+static int dev_alloc(hdgc_ctx* c, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) return set_err(HDGC_ENOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+  c->bytes += (int64_t)bytes;
+  return HDGC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// setup kernels (on-device geometry / adjacency precompute)
+
+// Per-element affine geometry: J = [v1-v0, v2-v0] (columns = edges, mesh2d.py:135-150),
+// Piola factor J/detJ and the V_h mass inverse 2/detJ.
+__global__ void geometry2d_kernel(const double* __restrict__ V, const int64_t* __restrict__ tri,
+                                  int nt, double* __restrict__ piola, double* __restrict__ minv,
+                                  int* __restrict__ bad) {
+  int T = blockIdx.x * blockDim.x + threadIdx.x;
+  if (T >= nt) return;
+  const int64_t a = tri[3 * (size_t)T], b = tri[3 * (size_t)T + 1], c = tri[3 * (size_t)T + 2];
+  const double x0 = V[2 * a], y0 = V[2 * a + 1];
+  const double j00 = V[2 * b] - x0, j10 = V[2 * b + 1] - y0;
+  const double j01 = V[2 * c] - x0, j11 = V[2 * c + 1] - y0;
+  const double det = j00 * j11 - j01 * j10;
+  if (!(det > 0.0)) atomicExch(bad, 1);
+  const double id = 1.0 / det;
+  piola[T] = j00 * id;
+  piola[(size_t)nt + T] = j01 * id;
+  piola[2 * (size_t)nt + T] = j10 * id;
+  piola[3 * (size_t)nt + T] = j11 * id;
+  minv[T] = 2.0 * id;
+}
+
+// boundary flag per facet
+__global__ void bflag_kernel(const int64_t* __restrict__ fe, int nfac, int* __restrict__ flag) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nfac) flag[f] = fe[2 * (size_t)f + 1] < 0 ? 1 : 0;
+}
+
+// in-place exclusive scan of n ints, single CTA of 1024 threads (setup only)
+__global__ void scan_kernel(int* __restrict__ a, int n, int* __restrict__ total) {
+  __shared__ int part[1024];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < n ? a[i] : 0;
+    part[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+      int t = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+      __syncthreads();
+      part[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (i < n) a[i] = carry + part[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += part[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+// element-owned neighbour codes from the facet arrays (mesh2d.py:178-207)
+__global__ void codes_kernel(const int64_t* __restrict__ fe, const int64_t* __restrict__ fl,
+                             const int* __restrict__ slot, int nfac, int faces_per_elem,
+                             int32_t* __restrict__ code, int* __restrict__ bad) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nfac) return;
+  const int64_t e0 = fe[2 * (size_t)f], e1 = fe[2 * (size_t)f + 1];
+  const int64_t l0 = fl[2 * (size_t)f], l1 = fl[2 * (size_t)f + 1];
+  if (e0 < 0 || l0 < 0 || l0 >= faces_per_elem) { atomicExch(bad, 2); return; }
+  if (e1 >= 0) {
+    if (l1 < 0 || l1 >= faces_per_elem) { atomicExch(bad, 2); return; }
+    code[e0 * faces_per_elem + l0] = (int32_t)((e1 << 2) | l1);
+    code[e1 * faces_per_elem + l1] = (int32_t)((e0 << 2) | l0);
+  } else {
+    code[e0 * faces_per_elem + l0] = -1 - slot[f];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// transfer kernels:  I (BDM -> V_h)  and  I^T (V_h functionals -> BDM-test)
+
+template <int K, bool TRANSPOSE>
+__global__ void __launch_bounds__(128)
+transfer2d_kernel(const double* __restrict__ tab, const double* __restrict__ piola, int nt,
+                  const double* __restrict__ in, double* __restrict__ out) {
+  using D = Dims<K>;
+  constexpr int NB = D::NB, NBS = D::NBS;
+  const int T = blockIdx.x * blockDim.x + threadIdx.x;
+  if (T >= nt) return;
+  const double* coef = tab + D::OFF_COEF;
+  const double P00 = piola[T], P01 = piola[(size_t)nt + T];
+  const double P10 = piola[2 * (size_t)nt + T], P11 = piola[3 * (size_t)nt + T];
+  double x[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) x[j] = in[(size_t)T * NB + j];
+  if (!TRANSPOSE) {
+    // w[c,m] = sum_d P[c][d] (coef u)[d,m]
+    double uh[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      double a = 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) a = fma(__ldg(coef + i * NB + j), x[j], a);
+      uh[i] = a;
+    }
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) {
+      out[(size_t)T * NB + m] = fma(P00, uh[m], P01 * uh[NBS + m]);
+      out[(size_t)T * NB + NBS + m] = fma(P10, uh[m], P11 * uh[NBS + m]);
+    }
+  } else {
+    double s[NB];
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) {
+      s[m] = fma(P00, x[m], P10 * x[NBS + m]);
+      s[NBS + m] = fma(P01, x[m], P11 * x[NBS + m]);
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      double a = 0.0;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) a = fma(__ldg(coef + i * NB + j), s[i], a);
+      out[(size_t)T * NB + j] = a;
+    }
+  }
+}
+
+// max |J u_hat / detJ| over elements x volume points (positive doubles order as uint64)
+template <int K>
+__global__ void __launch_bounds__(128)
+maxspeed2d_kernel(const double* __restrict__ tab, const double* __restrict__ piola, int nt,
+                  const double* __restrict__ u, unsigned long long* __restrict__ out) {
+  using D = Dims<K>;
+  constexpr int NB = D::NB, NBS = D::NBS;
+  const int T = blockIdx.x * blockDim.x + threadIdx.x;
+  double best = 0.0;
+  if (T < nt) {
+    const double* coef = tab + D::OFF_COEF;
+    const double* vD = tab + D::OFF_VD;
+    double uh[NB];
+    {
+      double x[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) x[j] = u[(size_t)T * NB + j];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) a = fma(__ldg(coef + i * NB + j), x[j], a);
+        uh[i] = a;
+      }
+    }
+    const double P00 = piola[T], P01 = piola[(size_t)nt + T];
+    const double P10 = piola[2 * (size_t)nt + T], P11 = piola[3 * (size_t)nt + T];
+    for (int q = 0; q < D::NQV; ++q) {
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) {
+        const double d = __ldg(vD + q * NBS + m);
+        a = fma(uh[m], d, a);
+        b = fma(uh[NBS + m], d, b);
+      }
+      const double x = fma(P00, a, P01 * b), y = fma(P10, a, P11 * b);
+      best = fmax(best, sqrt(fma(x, x, y * y)));
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+
+template <int K>
+static int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow,
+                       double* out, double dt, cudaStream_t st) {
+  ElemParams p;
+  p.tab = c->d_tab;
+  p.u = u;
+  p.w = w;
+  p.inflow = inflow;
+  p.code = c->d_code;
+  p.piola = c->d_piola;
+  p.minv = c->d_minv;
+  p.out = out;
+  p.dt = dt;
+  p.nt = c->nt;
+  const int threads = 128;
+  const int blocks = (c->nt + threads - 1) / threads;
+  const int smem = thread_smem_bytes<K>();
+  auto launch = [&](auto kern) -> int {
+    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<blocks, threads, smem, st>>>(p);
+    CUDA_TRY(cudaGetLastError());
+    return HDGC_OK;
+  };
+  switch (mode) {
+    case MODE_APPLY: return launch(conv2d_thread_kernel<K, MODE_APPLY>);
+    case MODE_SUBSTEP: return launch(conv2d_thread_kernel<K, MODE_SUBSTEP>);
+    default: return launch(conv2d_thread_kernel<K, MODE_APPLY_IT>);
+  }
+}
+
+template <int K>
+static int launch_transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st) {
+  const int threads = 128, blocks = (c->nt + threads - 1) / threads;
+  if (dir == 0) transfer2d_kernel<K, false><<<blocks, threads, 0, st>>>(c->d_tab, c->d_piola, c->nt, in, out);
+  else transfer2d_kernel<K, true><<<blocks, threads, 0, st>>>(c->d_tab, c->d_piola, c->nt, in, out);
+  CUDA_TRY(cudaGetLastError());
+  return HDGC_OK;
+}
+
+template <int K>
+static int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st) {
+  const int threads = 128, blocks = (c->nt + threads - 1) / threads;
+  CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
+  maxspeed2d_kernel<K><<<blocks, threads, 0, st>>>(c->d_tab, c->d_piola, c->nt, u,
+                                                   reinterpret_cast<unsigned long long*>(out));
+  CUDA_TRY(cudaGetLastError());
+  return HDGC_OK;
+}
+
+#define HDGC_K_SWITCH(k, CALL)                        \
+  switch (k) {                                        \
+    case 1: { constexpr int KK = 1; return CALL; }    \
+    case 2: { constexpr int KK = 2; return CALL; }    \
+    case 3: { constexpr int KK = 3; return CALL; }    \
+    case 4: { constexpr int KK = 4; return CALL; }    \
+    case 5: { constexpr int KK = 5; return CALL; }    \
+    case 6: { constexpr int KK = 6; return CALL; }    \
+    case 7: { constexpr int KK = 7; return CALL; }    \
+    case 8: { constexpr int KK = 8; return CALL; }    \
+    default: return set_err(HDGC_EUNSUP, "order k=%d not supported (1..8)", k); \
+  }
+
+static int elem(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
+                double dt, cudaStream_t st) {
+  HDGC_K_SWITCH(c->k, launch_elem<KK>(c, mode, u, w, inflow, out, dt, st));
+}
+
+static int transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st) {
+  HDGC_K_SWITCH(c->k, launch_transfer<KK>(c, dir, in, out, st));
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+const char* hdgc_last_error(void) { return g_err.c_str(); }
+const char* hdgc_version(void) { return "hdgconv 0.1 sm_100a fp64"; }
+
+int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ctx** out) {
+  if (!mesh || !tab || !out) return set_err(HDGC_EINVAL, "null argument");
+  *out = nullptr;
+  if (mesh->dim != 2) return set_err(HDGC_EUNSUP, "dim=%d not supported by this build", mesh->dim);
+  const int k = tab->k;
+  if (k < 1 || k > 8) return set_err(HDGC_EUNSUP, "order k=%d not supported (1..8)", k);
+  if (tab->nqv != dims_nqv(k) || tab->nf != dims_nf(k))
+    return set_err(HDGC_EINVAL, "table sizes nqv=%d nf=%d do not match the k=%d rules (%d, %d)",
+                   tab->nqv, tab->nf, k, dims_nqv(k), dims_nf(k));
+  if (mesh->n_elements <= 0 || mesh->n_vertices <= 0 || mesh->n_facets <= 0)
+    return set_err(HDGC_EINVAL, "empty mesh");
+  if ((int64_t)mesh->n_elements * 4 > INT32_MAX) return set_err(HDGC_EINVAL, "too many elements");
+  if (!mesh->vertices || !mesh->elements || !mesh->facet_elems || !mesh->facet_local || !tab->coef || !tab->div_modal ||
+      !tab->vol_w || !tab->vol_D || !tab->vol_G || !tab->fac_w || !tab->fac_L || !tab->fac_D || !tab->fac_len)
+    return set_err(HDGC_EINVAL, "null array in descriptor");
+
+  hdgc_ctx* c = new hdgc_ctx();
+  c->dim = 2;
+  c->k = k;
+  c->nbs = dims_nbs(k);
+  c->nb = 2 * c->nbs;
+  c->nqv = tab->nqv;
+  c->nf = tab->nf;
+  c->nt = mesh->n_elements;
+  c->nv = mesh->n_vertices;
+  c->nf_facets = mesh->n_facets;
+  c->variant = 0;
+
+  // pack tables (host), Dims<K> layout
+  const int nb = c->nb, nbs = c->nbs, nqv = c->nqv, nf = c->nf, ne = k + 1;
+  std::vector<double> h(dims_tab(k), 0.0);
+  size_t o = 0;
+  memcpy(&h[o], tab->coef, sizeof(double) * nb * nb); o += (size_t)nb * nb;
+  memcpy(&h[o], tab->div_modal, sizeof(double) * (k * (k + 1) / 2) * nb); o += (size_t)(k * (k + 1) / 2) * nb;
+  memcpy(&h[o], tab->vol_w, sizeof(double) * nqv); o += nqv;
+  memcpy(&h[o], tab->vol_D, sizeof(double) * nqv * nbs); o += (size_t)nqv * nbs;
+  memcpy(&h[o], tab->vol_G, sizeof(double) * nqv * nbs * 2); o += (size_t)nqv * nbs * 2;
+  memcpy(&h[o], tab->fac_w, sizeof(double) * nf); o += nf;
+  memcpy(&h[o], tab->fac_L, sizeof(double) * nf * ne); o += (size_t)nf * ne;
+  memcpy(&h[o], tab->fac_D, sizeof(double) * 3 * nf * nbs); o += (size_t)3 * nf * nbs;
+  memcpy(&h[o], tab->fac_len, sizeof(double) * 3);
+
+  int rc = HDGC_OK;
+  double* d_V = nullptr;
+  int64_t *d_tri = nullptr, *d_fe = nullptr, *d_fl = nullptr;
+  int *d_slot = nullptr, *d_flag = nullptr;
+  const size_t NT = c->nt, NF = c->nf_facets;
+  auto fail = [&](int code) {
+    cudaFree(d_V); cudaFree(d_tri); cudaFree(d_fe); cudaFree(d_fl); cudaFree(d_slot); cudaFree(d_flag);
+    hdgc_destroy(c);
+    return code;
+  };
+  if ((rc = dev_alloc(c, (void**)&c->d_tab, h.size() * sizeof(double)))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&c->d_code, NT * 3 * sizeof(int32_t)))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&c->d_piola, NT * 4 * sizeof(double)))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&c->d_minv, NT * sizeof(double)))) return fail(rc);
+  if ((rc = dev_alloc(c, (void**)&c->d_scratch, NT * nb * sizeof(double)))) return fail(rc);
+#define SETUP_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) \
+    return fail(set_err(HDGC_ECUDA, "%s: %s", #x, cudaGetErrorString(e_))); } while (0)
+  SETUP_TRY(cudaMemcpy(c->d_tab, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+  SETUP_TRY(cudaMalloc(&d_V, sizeof(double) * 2 * c->nv));
+  SETUP_TRY(cudaMalloc(&d_tri, sizeof(int64_t) * 3 * NT));
+  SETUP_TRY(cudaMalloc(&d_fe, sizeof(int64_t) * 2 * NF));
+  SETUP_TRY(cudaMalloc(&d_fl, sizeof(int64_t) * 2 * NF));
+  SETUP_TRY(cudaMalloc(&d_slot, sizeof(int) * (NF + 2)));
+  SETUP_TRY(cudaMemcpy(d_V, mesh->vertices, sizeof(double) * 2 * c->nv, cudaMemcpyHostToDevice));
+  SETUP_TRY(cudaMemcpy(d_tri, mesh->elements, sizeof(int64_t) * 3 * NT, cudaMemcpyHostToDevice));
+  SETUP_TRY(cudaMemcpy(d_fe, mesh->facet_elems, sizeof(int64_t) * 2 * NF, cudaMemcpyHostToDevice));
+  SETUP_TRY(cudaMemcpy(d_fl, mesh->facet_local, sizeof(int64_t) * 2 * NF, cudaMemcpyHostToDevice));
+  int* d_misc = d_slot + NF;  // [0] = total boundary facets, [1] = bad flag
+  SETUP_TRY(cudaMemset(d_misc, 0, 2 * sizeof(int)));
+  SETUP_TRY(cudaMemset(c->d_code, 0x80, NT * 3 * sizeof(int32_t)));  // sentinel: unmatched
+  {
+    const int th = 256;
+    geometry2d_kernel<<<(int)((NT + th - 1) / th), th>>>(d_V, d_tri, (int)NT, c->d_piola, c->d_minv, d_misc + 1);
+    bflag_kernel<<<(int)((NF + th - 1) / th), th>>>(d_fe, (int)NF, d_slot);
+    scan_kernel<<<1, 1024>>>(d_slot, (int)NF, d_misc);
+    codes_kernel<<<(int)((NF + th - 1) / th), th>>>(d_fe, d_fl, d_slot, (int)NF, 3, c->d_code, d_misc + 1);
+    SETUP_TRY(cudaGetLastError());
+  }
+  int misc[2];
+  SETUP_TRY(cudaMemcpy(misc, d_misc, sizeof(misc), cudaMemcpyDeviceToHost));
+  if (misc[1] == 1) return fail(set_err(HDGC_EINVAL, "inverted or degenerate element (detJ <= 0)"));
+  if (misc[1] == 2) return fail(set_err(HDGC_EINVAL, "invalid facet_elems/facet_local entry"));
+  c->nbf = misc[0];
+  cudaFree(d_V); cudaFree(d_tri); cudaFree(d_fe); cudaFree(d_fl); cudaFree(d_slot);
+  *out = c;
+  return HDGC_OK;
+#undef SETUP_TRY
+}
+
+int hdgc_destroy(hdgc_ctx* c) {
+  if (!c) return HDGC_OK;
+  cudaFree(c->d_tab); cudaFree(c->d_code); cudaFree(c->d_piola); cudaFree(c->d_minv);
+  cudaFree(c->d_scratch); cudaFree(c->d_hu); cudaFree(c->d_hw); cudaFree(c->d_hr); cudaFree(c->d_hin);
+  delete c;
+  return HDGC_OK;
+}
+
+int hdgc_get_info(const hdgc_ctx* c, hdgc_info* info) {
+  if (!c || !info) return set_err(HDGC_EINVAL, "null argument");
+  info->dim = c->dim; info->k = c->k; info->nb = c->nb; info->nbs = c->nbs;
+  info->nqv = c->nqv; info->nf = c->nf;
+  info->n_elements = c->nt; info->n_facets = c->nf_facets; info->n_boundary_facets = c->nbf;
+  info->volume_variant = c->variant;
+  info->device_bytes = c->bytes;
+  return HDGC_OK;
+}
+
+int hdgc_apply_v(hdgc_ctx* c, const double* u, const double* w, const double* inflow, double* r, void* stream) {
+  if (!c || !u || !w || !r) return set_err(HDGC_EINVAL, "null argument");
+  if (r == u || r == w || r == inflow) return set_err(HDGC_EINVAL, "output aliases an input");
+  return elem(c, MODE_APPLY, u, w, inflow, r, 0.0, (cudaStream_t)stream);
+}
+
+int hdgc_apply_w(hdgc_ctx* c, const double* u, const double* inflow, double* r_w, void* stream) {
+  if (!c || !u || !r_w) return set_err(HDGC_EINVAL, "null argument");
+  if (r_w == u || r_w == inflow) return set_err(HDGC_EINVAL, "output aliases an input");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = transfer(c, 0, u, c->d_scratch, st);
+  if (rc) return rc;
+  return elem(c, MODE_APPLY_IT, u, c->d_scratch, inflow, r_w, 0.0, st);
+}
+
+int hdgc_substeps(hdgc_ctx* c, const double* u, double* w, const double* inflow, double dt, int32_t nsteps,
+                  void* stream) {
+  if (!c || !u || !w) return set_err(HDGC_EINVAL, "null argument");
+  if (nsteps < 0) return set_err(HDGC_EINVAL, "nsteps < 0");
+  if (w == u || w == inflow) return set_err(HDGC_EINVAL, "w aliases an input");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* a = w;
+  double* b = c->d_scratch;
+  for (int s = 0; s < nsteps; ++s) {
+    int rc = elem(c, MODE_SUBSTEP, u, a, inflow, b, dt, st);
+    if (rc) return rc;
+    double* t = a; a = b; b = t;
+  }
+  if (a != w) CUDA_TRY(cudaMemcpyAsync(w, a, sizeof(double) * (size_t)c->nt * c->nb, cudaMemcpyDeviceToDevice, st));
+  return HDGC_OK;
+}
+
+int hdgc_transfer(hdgc_ctx* c, int32_t direction, const double* in, double* out, void* stream) {
+  if (!c || !in || !out) return set_err(HDGC_EINVAL, "null argument");
+  if (in == out) return set_err(HDGC_EINVAL, "output aliases input");
+  if (direction != 0 && direction != 1) return set_err(HDGC_EINVAL, "direction must be 0 (I) or 1 (I^T)");
+  return transfer(c, direction, in, out, (cudaStream_t)stream);
+}
+
+int hdgc_mass_inverse(hdgc_ctx* c, double* out, void* stream) {
+  if (!c || !out) return set_err(HDGC_EINVAL, "null argument");
+  CUDA_TRY(cudaMemcpyAsync(out, c->d_minv, sizeof(double) * c->nt, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return HDGC_OK;
+}
+
+int hdgc_max_speed(hdgc_ctx* c, const double* u, double* out_dev, void* stream) {
+  if (!c || !u || !out_dev) return set_err(HDGC_EINVAL, "null argument");
+  HDGC_K_SWITCH(c->k, launch_maxspeed<KK>(c, u, out_dev, (cudaStream_t)stream));
+}
+
+static int ensure_staging(hdgc_ctx* c, bool need_inflow) {
+  const size_t vec = sizeof(double) * (size_t)c->nt * c->nb;
+  int rc;
+  if (!c->d_hu && (rc = dev_alloc(c, (void**)&c->d_hu, vec))) return rc;
+  if (!c->d_hw && (rc = dev_alloc(c, (void**)&c->d_hw, vec))) return rc;
+  if (!c->d_hr && (rc = dev_alloc(c, (void**)&c->d_hr, vec))) return rc;
+  if (need_inflow && !c->d_hin && c->nbf > 0 &&
+      (rc = dev_alloc(c, (void**)&c->d_hin, sizeof(double) * (size_t)c->nbf * c->nf * 2)))
+    return rc;
+  return HDGC_OK;
+}
+
+int hdgc_apply_v_host(hdgc_ctx* c, const double* u, const double* w, const double* inflow, double* r, void* stream) {
+  if (!c || !u || !w || !r) return set_err(HDGC_EINVAL, "null argument");
+  int rc = ensure_staging(c, inflow != nullptr);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t vec = sizeof(double) * (size_t)c->nt * c->nb;
+  CUDA_TRY(cudaMemcpyAsync(c->d_hu, u, vec, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->d_hw, w, vec, cudaMemcpyHostToDevice, st));
+  const double* din = nullptr;
+  if (inflow && c->nbf > 0) {
+    CUDA_TRY(cudaMemcpyAsync(c->d_hin, inflow, sizeof(double) * (size_t)c->nbf * c->nf * 2, cudaMemcpyHostToDevice, st));
+    din = c->d_hin;
+  }
+  if ((rc = elem(c, MODE_APPLY, c->d_hu, c->d_hw, din, c->d_hr, 0.0, st))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(r, c->d_hr, vec, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return HDGC_OK;
+}
+
+int hdgc_substeps_host(hdgc_ctx* c, const double* u, double* w, const double* inflow, double dt, int32_t nsteps,
+                       void* stream) {
+  if (!c || !u || !w) return set_err(HDGC_EINVAL, "null argument");
+  int rc = ensure_staging(c, inflow != nullptr);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t vec = sizeof(double) * (size_t)c->nt * c->nb;
+  CUDA_TRY(cudaMemcpyAsync(c->d_hu, u, vec, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->d_hw, w, vec, cudaMemcpyHostToDevice, st));
+  const double* din = nullptr;
+  if (inflow && c->nbf > 0) {
+    CUDA_TRY(cudaMemcpyAsync(c->d_hin, inflow, sizeof(double) * (size_t)c->nbf * c->nf * 2, cudaMemcpyHostToDevice, st));
+    din = c->d_hin;
+  }
+  if ((rc = hdgc_substeps(c, c->d_hu, c->d_hw, din, dt, nsteps, stream))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(w, c->d_hw, vec, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return HDGC_OK;
+}
+
+}  // extern "C"

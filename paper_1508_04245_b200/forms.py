@@ -1,0 +1,344 @@
+"""Drop-in host interface for the convection path (mirrors ``forms`` in SPEC).
+
+Reference interface (module ``forms``):
+
+* ``apply_convection(u_conv, w, data) -> residual over V_h``
+* ``apply_transfer(direction in {I, I_transpose}, vec)``
+* ``assemble_mass(spaces, which='M_V')``  (diagonal on affine)
+
+Same argument order and meaning; the arithmetic runs in the CUDA library
+``libhdgconv.so`` (include/hdgconv.h) — there is no CPU path.  Inputs may be
+torch CUDA fp64 tensors (zero copy, asynchronous on the current stream) or
+numpy arrays (copied in, result copied out).  Layouts are element-local
+(SURVEY.md A.1): ``u`` (NT, nb) BDM coefficients, ``w``/``r`` (NT, nb) V_h
+coefficients with index c*nbs+m.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from . import basis as B
+
+__all__ = ["FESpace", "FEField", "ConvectionData", "ConvectionOperator", "operator_for",
+           "apply_convection", "apply_convection_W", "apply_transfer", "assemble_mass",
+           "device_tables"]
+
+
+# ---------------------------------------------------------------------------
+# spaces / fields (the subset of fespace.FESpace / FEField the path needs,
+# SPEC.md:177-199)
+
+
+@dataclass(frozen=True)
+class FESpace:
+    """kind in {'Hdiv', 'VectorDG'}; element-local layouts of size nb per element."""
+
+    mesh: object
+    kind: str
+    k: int
+
+    @property
+    def nb(self) -> int:
+        return B.nb_of(self.k)
+
+    @property
+    def ndof(self) -> int:
+        # element-local storage; VectorDG matches SPEC.md:183 exactly
+        return self.mesh.n_elements * self.nb
+
+
+@dataclass
+class FEField:
+    space: FESpace
+    coeffs: object          # (NT, nb) numpy array or torch CUDA tensor
+
+
+@dataclass
+class ConvectionData:
+    """t-dependent data of apply_convection: the exterior (Dirichlet) value
+    on boundary facets, (NBF, nf, 2) at quad_interval(3k+1) points
+    (SPEC.md:302).  ``inflow=None`` means no inflow data (own trace)."""
+
+    inflow: object = None
+    t: float = 0.0
+
+
+# ---------------------------------------------------------------------------
+# tables
+
+
+def device_tables(k: int) -> dict:
+    """Reference tables uploaded once per context."""
+    bdm = B.build_bdm_basis(k)
+    qv = B.volume_rule(k)
+    qf = B.facet_rule(k)
+    D, G = B.dubiner_values(k, qv.points, with_grads=True)
+    fD = np.stack([B.dubiner_values(k, B.ref_edge_points(e, qf.points)) for e in range(3)])
+    return {
+        "coef": np.ascontiguousarray(bdm.coef),
+        "div_modal": np.ascontiguousarray(B.bdm_divergence_modal(k)),
+        "vol_w": np.ascontiguousarray(qv.weights),
+        "vol_D": np.ascontiguousarray(D),
+        "vol_G": np.ascontiguousarray(G),
+        "fac_w": np.ascontiguousarray(qf.weights),
+        "fac_L": np.ascontiguousarray(B.legendre_values(k, qf.points)),
+        "fac_D": np.ascontiguousarray(fD),
+        "fac_len": np.ascontiguousarray(B.REF_EDGE_LENGTHS),
+        "nqv": qv.weights.size,
+        "nf": qf.weights.size,
+    }
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+# ---------------------------------------------------------------------------
+# device context
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class ConvectionOperator:
+    """Device context for C^V on one affine mesh and order k.
+
+    Owns the uploaded tables, the on-device geometry (Piola factors J/detJ,
+    2/detJ) and the element-owned neighbour codes; compute calls allocate
+    nothing except their outputs.
+    """
+
+    def __init__(self, mesh, k: int):
+        lib = _lib.load()
+        self.mesh = mesh
+        self.k = int(k)
+        self.nb = B.nb_of(k)
+        self.nbs = B.nbs_of(k)
+        tab = device_tables(k)
+        self.nf = tab["nf"]
+        self.nqv = tab["nqv"]
+        keep = []
+
+        def arr(x, dt=np.float64):
+            a = np.ascontiguousarray(x, dtype=dt)
+            keep.append(a)
+            return _ptr(a)
+
+        md = _lib.MeshDesc(
+            dim=2, n_vertices=len(mesh.vertices), n_elements=mesh.n_elements,
+            n_facets=mesh.n_facets, vertices=arr(mesh.vertices), elements=arr(mesh.triangles, np.int64),
+            facet_elems=arr(mesh.facet_elems, np.int64), facet_local=arr(mesh.facet_local, np.int64),
+            facet_perm=None)
+        td = _lib.TablesDesc(
+            k=self.k, nqv=self.nqv, nf=self.nf, coef=arr(tab["coef"]), div_modal=arr(tab["div_modal"]), vol_w=arr(tab["vol_w"]),
+            vol_D=arr(tab["vol_D"]), vol_G=arr(tab["vol_G"]), fac_w=arr(tab["fac_w"]),
+            fac_L=arr(tab["fac_L"]), fac_D=arr(tab["fac_D"]), fac_len=arr(tab["fac_len"]))
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("ConvectionOperator needs a CUDA device (no CPU fallback)")
+        torch.cuda.init()
+        h = C.c_void_p()
+        _lib.check(lib.hdgc_create(C.byref(md), C.byref(td), C.byref(h)), "hdgc_create")
+        self._h = h
+        self._fin = weakref.finalize(self, lib.hdgc_destroy, h)
+        info = _lib.Info()
+        _lib.check(lib.hdgc_get_info(h, C.byref(info)), "hdgc_get_info")
+        self.info = info
+        self.n_elements = info.n_elements
+        self.n_boundary_facets = info.n_boundary_facets
+
+    # -- helpers ---------------------------------------------------------------
+
+    @property
+    def handle(self):
+        return self._h
+
+    @staticmethod
+    def _stream():
+        return C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+    def _dev(self, x, shape, name):
+        torch = _torch()
+        if isinstance(x, torch.Tensor):
+            if not x.is_cuda or x.dtype != torch.float64:
+                raise TypeError(f"{name}: expected a CUDA float64 tensor")
+            t = x.contiguous()
+            host = False
+        else:
+            a = np.ascontiguousarray(x, dtype=np.float64)
+            t = torch.from_numpy(a).cuda()
+            host = True
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name}: shape {tuple(t.shape)} != {tuple(shape)}")
+        return t, host
+
+    def _vec_shape(self):
+        return (self.n_elements, self.nb)
+
+    def _inflow(self, inflow):
+        if inflow is None:
+            return None, None
+        t, _ = self._dev(inflow, (self.n_boundary_facets, self.nf, 2), "inflow")
+        return t, C.c_void_p(t.data_ptr())
+
+    # -- operators -------------------------------------------------------------
+
+    def apply(self, u, w, inflow=None, out=None):
+        """r = C^V(u; w)."""
+        torch = _torch()
+        lib = _lib.load()
+        ut, host = self._dev(u, self._vec_shape(), "u_conv")
+        wt, host2 = self._dev(w, self._vec_shape(), "w")
+        it, ip = self._inflow(inflow)
+        r = out if out is not None else torch.empty_like(wt)
+        _lib.check(lib.hdgc_apply_v(self._h, C.c_void_p(ut.data_ptr()), C.c_void_p(wt.data_ptr()), ip,
+                                    C.c_void_p(r.data_ptr()), self._stream()), "hdgc_apply_v")
+        return r.cpu().numpy() if (host and host2 and out is None) else r
+
+    def apply_host(self, u: np.ndarray, w: np.ndarray, inflow: Optional[np.ndarray] = None) -> np.ndarray:
+        """End-to-end apply on host arrays through hdgc_apply_v_host (H2D,
+        kernel, D2H inside the library)."""
+        lib = _lib.load()
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        r = np.empty_like(w)
+        ip = None
+        if inflow is not None:
+            inflow = np.ascontiguousarray(inflow, dtype=np.float64)
+            ip = _ptr(inflow)
+        _lib.check(lib.hdgc_apply_v_host(self._h, _ptr(u), _ptr(w), ip, _ptr(r), self._stream()),
+                   "hdgc_apply_v_host")
+        return r
+
+    def apply_w(self, u, inflow=None, out=None):
+        """r_W = I^T C^V(u; I u) in BDM-test layout."""
+        torch = _torch()
+        lib = _lib.load()
+        ut, host = self._dev(u, self._vec_shape(), "u_conv")
+        it, ip = self._inflow(inflow)
+        r = out if out is not None else torch.empty_like(ut)
+        _lib.check(lib.hdgc_apply_w(self._h, C.c_void_p(ut.data_ptr()), ip, C.c_void_p(r.data_ptr()),
+                                    self._stream()), "hdgc_apply_w")
+        return r.cpu().numpy() if (host and out is None) else r
+
+    def transfer(self, vec, transpose: bool = False):
+        """I vec (BDM -> V_h) or I^T vec."""
+        torch = _torch()
+        lib = _lib.load()
+        xt, host = self._dev(vec, self._vec_shape(), "vec")
+        y = torch.empty_like(xt)
+        _lib.check(lib.hdgc_transfer(self._h, 1 if transpose else 0, C.c_void_p(xt.data_ptr()),
+                                     C.c_void_p(y.data_ptr()), self._stream()), "hdgc_transfer")
+        return y.cpu().numpy() if host else y
+
+    def substeps(self, u, w, dt: float, nsteps: int, inflow=None):
+        """nsteps forward-Euler substeps of dw/ds = -(M^V)^{-1} C^V(u) w, u frozen,
+        device-resident.  Torch input is updated in place."""
+        lib = _lib.load()
+        ut, _ = self._dev(u, self._vec_shape(), "u_conv")
+        wt, host = self._dev(w, self._vec_shape(), "w")
+        it, ip = self._inflow(inflow)
+        if not host and wt.data_ptr() != w.data_ptr():
+            raise ValueError("w must be contiguous for the in-place substep loop")
+        _lib.check(lib.hdgc_substeps(self._h, C.c_void_p(ut.data_ptr()), C.c_void_p(wt.data_ptr()), ip,
+                                     C.c_double(dt), C.c_int32(nsteps), self._stream()), "hdgc_substeps")
+        return wt.cpu().numpy() if host else wt
+
+    def substeps_host(self, u: np.ndarray, w: np.ndarray, dt: float, nsteps: int,
+                      inflow: Optional[np.ndarray] = None) -> np.ndarray:
+        """End-to-end substep batch on host arrays (hdgc_substeps_host)."""
+        lib = _lib.load()
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.array(w, dtype=np.float64, copy=True, order="C")
+        ip = None
+        if inflow is not None:
+            inflow = np.ascontiguousarray(inflow, dtype=np.float64)
+            ip = _ptr(inflow)
+        _lib.check(lib.hdgc_substeps_host(self._h, _ptr(u), _ptr(out), ip, C.c_double(dt),
+                                          C.c_int32(nsteps), self._stream()), "hdgc_substeps_host")
+        return out
+
+    def mass_inverse(self):
+        """(M^V)^{-1} diagonal: 2/detJ per element."""
+        torch = _torch()
+        lib = _lib.load()
+        out = torch.empty(self.n_elements, dtype=torch.float64, device="cuda")
+        _lib.check(lib.hdgc_mass_inverse(self._h, C.c_void_p(out.data_ptr()), self._stream()),
+                   "hdgc_mass_inverse")
+        return out
+
+    def max_speed(self, u) -> float:
+        """max |u| over elements x volume points (for the CFL substep)."""
+        torch = _torch()
+        lib = _lib.load()
+        ut, _ = self._dev(u, self._vec_shape(), "u_conv")
+        out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        _lib.check(lib.hdgc_max_speed(self._h, C.c_void_p(ut.data_ptr()), C.c_void_p(out.data_ptr()),
+                                      self._stream()), "hdgc_max_speed")
+        return float(out.item())
+
+
+_CACHE: dict = {}
+
+
+def operator_for(mesh, k: int) -> ConvectionOperator:
+    """Context cache keyed by (mesh identity, k): building a context uploads
+    tables and runs the geometry precompute, so do it once."""
+    key = (id(mesh), int(k))
+    op = _CACHE.get(key)
+    if op is None or op.mesh is not mesh:
+        op = ConvectionOperator(mesh, k)
+        _CACHE[key] = op
+    return op
+
+
+# ---------------------------------------------------------------------------
+# reference-named entry points
+
+
+def apply_convection(u_conv: FEField, w, data: Optional[ConvectionData] = None):
+    """``forms.apply_convection(u_conv, w, data)``.
+
+    u_conv: FEField over Hdiv(k) (element-local BDM coefficients);
+    w: V_h coefficients (NT, nb) (array/tensor or FEField over VectorDG(k));
+    data: ConvectionData (inflow values).  Returns the residual r over V_h.
+    Pure: inputs are not modified.  Errors: none beyond argument checks.
+    """
+    sp = u_conv.space
+    op = operator_for(sp.mesh, sp.k)
+    wc = w.coeffs if isinstance(w, FEField) else w
+    inflow = None if data is None else data.inflow
+    return op.apply(u_conv.coeffs, wc, inflow)
+
+
+def apply_convection_W(u_conv: FEField, data: Optional[ConvectionData] = None):
+    """C^U u = I^T C^V(u; I u) in the BDM-test layout."""
+    sp = u_conv.space
+    op = operator_for(sp.mesh, sp.k)
+    return op.apply_w(u_conv.coeffs, None if data is None else data.inflow)
+
+
+def apply_transfer(direction: str, vec, space: FESpace):
+    """``forms.apply_transfer``: direction 'I' maps BDM
+    coefficients to V_h, 'I_transpose' maps V_h functionals to BDM-test."""
+    if direction not in ("I", "I_transpose"):
+        raise ValueError(f"unknown transfer direction {direction!r}")
+    return operator_for(space.mesh, space.k).transfer(vec, transpose=direction == "I_transpose")
+
+
+def assemble_mass(space: FESpace, which: str = "M_V"):
+    """Diagonal M^V on affine meshes: detJ/2 per element and mode
+    (SPEC.md:280-289), returned as its (NT,) inverse
+    scale 2/detJ as a CUDA tensor."""
+    if which != "M_V":
+        raise ValueError("only the V_h mass (M_V) is part of the convection path")
+    return operator_for(space.mesh, space.k).mass_inverse()

@@ -1,0 +1,63 @@
+"""C-ABI library: loads, exports every symbol include/hdgconv.h declares, and
+rejects bad arguments with status codes + last-error text — no GPU needed."""
+
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_1508_04245_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "hdgconv.h")).read()
+    return sorted(set(re.findall(r"\b(hdgc_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_header_symbols():
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.SYMBOLS)
+
+
+def test_version_and_error_paths():
+    lib = _lib.load()
+    assert b"sm_100a" in lib.hdgc_version()
+    h = C.c_void_p()
+    rc = lib.hdgc_create(None, None, C.byref(h))
+    assert rc == -1 and b"null" in lib.hdgc_last_error()
+    md = _lib.MeshDesc(dim=5)
+    td = _lib.TablesDesc(k=4)
+    assert lib.hdgc_create(C.byref(md), C.byref(td), C.byref(h)) == -4    # unsupported dim
+    md.dim = 2
+    td.k = 12
+    assert lib.hdgc_create(C.byref(md), C.byref(td), C.byref(h)) == -4    # unsupported order
+    td.k, td.nqv, td.nf = 4, 35, 7
+    assert lib.hdgc_create(C.byref(md), C.byref(td), C.byref(h)) == -1    # wrong rule size
+    assert b"nqv" in lib.hdgc_last_error()
+    assert lib.hdgc_apply_v(None, None, None, None, None, None) == -1
+    assert lib.hdgc_destroy(None) == 0
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    monkeypatch.setattr(_lib, "_LIB", None)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        _lib.load(str(tmp_path / "nope.so"))
+    monkeypatch.setattr(_lib, "_LIB", None)
+    _lib.load()
+
+
+def test_operator_refuses_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1508_04245_b200 import mesh as M
+    from paper_1508_04245_b200.forms import ConvectionOperator
+    with pytest.raises(RuntimeError, match="CUDA"):
+        ConvectionOperator(M.generate_structured((0, 0, 1, 1), 2, 2), 2)

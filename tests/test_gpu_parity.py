@@ -1,0 +1,188 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle.
+
+Tolerances are the north star's: relative l2 <= 1e-12 per apply, <= 1e-10
+after 100 substeps (BASELINE.json north_star).  The reference for small cases
+is the committed golden vectors computed on the REFERENCE's tables
+(tests/golden); at BASELINE's full sizes it is the oracle's C port
+(flux-difference form, fp64, pinned to long double by test_oracle.py).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import convection as O  # noqa: E402
+from oracle import port as P  # noqa: E402
+from paper_1508_04245_b200 import basis as B  # noqa: E402
+from paper_1508_04245_b200 import fields as F  # noqa: E402
+from paper_1508_04245_b200 import mesh as M  # noqa: E402
+from paper_1508_04245_b200.forms import (ConvectionData, ConvectionOperator, FEField, FESpace,  # noqa: E402
+                                         apply_convection, apply_convection_W, apply_transfer)
+from paper_1508_04245_b200.timeloop import propagate_convection  # noqa: E402
+
+APPLY_TOL = 1e-12
+SUBSTEP_TOL = 1e-10
+CASES = ["cfg1"] + [f"sweep_k{k}" for k in range(1, 9)] + ["jit_k3", "jit_k6", "sub_k4"]
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else a
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _case(name):
+    g = load_golden(f"conv_{name}.npz")
+    m = M.build_mesh(g["vertices"], g["triangles"])
+    inflow = g["inflow"] if "inflow" in g.files else None
+    return g, m, int(g["k"]), inflow
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_apply_vs_golden(name):
+    g, m, k, inflow = _case(name)
+    op = ConvectionOperator(m, k)
+    infd = None if inflow is None else dev(inflow)
+    r = op.apply(dev(g["u"]), dev(g["w"]), infd)
+    assert rel(r, g["r_ld"]) < APPLY_TOL
+    assert rel(r, g["r"]) < APPLY_TOL          # the textbook-form golden too
+    rr = op.apply(dev(g["u"]), dev(g["w_rand"]), infd)
+    assert rel(rr, g["r_rand_ld"]) < APPLY_TOL
+
+
+@pytest.mark.parametrize("name", ["jit_k3", "jit_k6", "sub_k4"])
+def test_substeps_vs_golden(name):
+    g, m, k, inflow = _case(name)
+    op = ConvectionOperator(m, k)
+    w = dev(g["w"])
+    op.substeps(dev(g["u"]), w, float(g["dt"]), int(g["nsub"]), None if inflow is None else dev(inflow))
+    assert rel(w, g["w_sub_ld"]) < SUBSTEP_TOL
+    assert rel(w, g["w_sub"]) < SUBSTEP_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg1", "sweep_k5", "jit_k6"])
+def test_transfer_and_apply_w(name):
+    g, m, k, inflow = _case(name)
+    op = ConvectionOperator(m, k)
+    assert rel(op.transfer(dev(g["u"])), g["w"]) < 1e-13
+    f = np.random.default_rng(0).standard_normal(g["w"].shape)
+    assert rel(op.transfer(dev(f), transpose=True), O.transfer_IT(m, k, f)) < 1e-13
+    rw = op.apply_w(dev(g["u"]), None if inflow is None else dev(inflow))
+    ref = O.transfer_IT(m, k, g["r_ld"])
+    assert rel(rw, ref) < APPLY_TOL
+
+
+def test_reference_named_entry_points():
+    g, m, k, inflow = _case("jit_k3")
+    sp = FESpace(m, "Hdiv", k)
+    uf = FEField(sp, g["u"])
+    r = apply_convection(uf, g["w"], ConvectionData(inflow=inflow))     # numpy in -> numpy out
+    assert isinstance(r, np.ndarray) and rel(r, g["r_ld"]) < APPLY_TOL
+    rw = apply_convection_W(uf, ConvectionData(inflow=inflow))
+    assert rel(rw, O.transfer_IT(m, k, g["r_ld"])) < APPLY_TOL
+    assert rel(apply_transfer("I", g["u"], sp), g["w"]) < 1e-13
+    v, nsub, ds = propagate_convection(g["w"], 0.0, float(g["dt"]) * int(g["nsub"]), uf,
+                                       ConvectionData(inflow=inflow), dt=float(g["dt"]))
+    assert nsub == int(g["nsub"]) and rel(v, g["w_sub_ld"]) < SUBSTEP_TOL
+
+
+def test_host_variants_match_device():
+    g, m, k, inflow = _case("sub_k4")
+    op = ConvectionOperator(m, k)
+    rd = op.apply(dev(g["u"]), dev(g["w"]), dev(inflow)).cpu().numpy()
+    rh = op.apply_host(g["u"], g["w"], inflow)
+    assert np.array_equal(rd, rh)
+    wh = op.substeps_host(g["u"], g["w"], float(g["dt"]), int(g["nsub"]), inflow)
+    assert rel(wh, g["w_sub_ld"]) < SUBSTEP_TOL
+
+
+def test_deterministic_bitwise():
+    g, m, k, inflow = _case("jit_k6")
+    op = ConvectionOperator(m, k)
+    a = op.apply(dev(g["u"]), dev(g["w_rand"]), dev(inflow)).cpu().numpy()
+    for _ in range(3):
+        b = op.apply(dev(g["u"]), dev(g["w_rand"]), dev(inflow)).cpu().numpy()
+        assert np.array_equal(a, b)
+
+
+def test_max_speed_and_mass():
+    m = M.generate_jittered(16, 0.2, 2)
+    k = 4
+    u = F.interpolate_curl(m, k, F.StreamFunction(6, 3, (1.0, 0.3)))
+    op = ConvectionOperator(m, k)
+    assert abs(op.max_speed(dev(u)) - F.max_speed_host(m, k, u)) < 1e-12 * F.max_speed_host(m, k, u)
+    assert rel(op.mass_inverse(), O.mass_inverse(m)) < 1e-15
+
+
+def test_edge_cases():
+    # single element, all facets on the boundary, with and without inflow
+    m = M.build_mesh(np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]]), np.array([[0, 1, 2]]))
+    for k in (1, 4, 8):
+        op = ConvectionOperator(m, k)
+        rng = np.random.default_rng(k)
+        u = rng.standard_normal((1, B.nb_of(k)))
+        w = rng.standard_normal((1, B.nb_of(k)))
+        inf = rng.standard_normal((3, B.facet_rule(k).weights.size, 2))
+        for data in (None, inf):
+            ref = O.apply_convection_flux_form(m, k, u, w, data).astype(float)
+            assert rel(op.apply(dev(u), dev(w), None if data is None else dev(data)), ref) < APPLY_TOL
+        # zero velocity -> zero output
+        assert np.abs(op.apply(dev(np.zeros_like(u)), dev(w)).cpu().numpy()).max() == 0.0
+    # bad arguments fail loudly
+    with pytest.raises(ValueError):
+        op.apply(dev(np.zeros((2, B.nb_of(8)))), dev(np.zeros((2, B.nb_of(8)))))
+    with pytest.raises(RuntimeError):
+        w = dev(np.zeros((1, B.nb_of(8))))
+        op.apply(w, w, out=w)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE full sizes vs the oracle's C port
+
+def _full(n, k, modes, seed, wind=(0.0, 0.0), jitter=None):
+    m = M.generate_jittered(n, 0.2, jitter) if jitter is not None else M.generate_structured((0, 0, 1, 1), n, n)
+    sf = F.StreamFunction(modes, seed, wind)
+    u = F.interpolate_curl(m, k, sf)
+    return m, sf, u, F.transfer_I_host(m, k, u), F.inflow_values(m, k, sf)
+
+
+def test_cfg2_apply_and_100_substeps():
+    m, sf, u, w, inf = _full(256, 4, 16, 2)
+    op = ConvectionOperator(m, k=4)
+    port = P.PortOperator(m, 4)
+    ud, wd, infd = dev(u), dev(w), dev(inf)
+    assert rel(op.apply(ud, wd, infd), port.apply(u, w, inf)) < APPLY_TOL
+    dt = F.cfl_dt(m.h_min(), 4, F.max_speed_host(m, 4, u))
+    op.substeps(ud, wd, dt, 100, infd)
+    ref = port.substeps(u, w, dt, 100, inf)
+    assert rel(wd, ref) < SUBSTEP_TOL
+    # random w, no cancellation: the textbook oracle itself agrees at full size
+    x = np.random.default_rng(7).standard_normal(w.shape)
+    assert rel(op.apply(ud, dev(x), infd), O.apply_convection(m, 4, u, x, inf)) < APPLY_TOL
+
+
+@pytest.mark.slow
+def test_cfg3_apply_and_50_substeps():
+    m, sf, u, w, inf = _full(512, 6, 32, 3, (1.0, 0.3), jitter=11)
+    op = ConvectionOperator(m, 6)
+    port = P.PortOperator(m, 6)
+    ud, wd, infd = dev(u), dev(w), dev(inf)
+    assert rel(op.apply(ud, wd, infd), port.apply(u, w, inf)) < APPLY_TOL
+    dt = F.cfl_dt(m.h_min(), 6, F.max_speed_host(m, 6, u))
+    op.substeps(ud, wd, dt, 50, infd)
+    assert rel(wd, port.substeps(u, w, dt, 50, inf)) < SUBSTEP_TOL
+
+
+@pytest.mark.parametrize("k", range(1, 9))
+def test_cfg4_order_sweep(k):
+    m, sf, u, w, inf = _full(128, k, 16, 2)
+    op = ConvectionOperator(m, k)
+    r = op.apply(dev(u), dev(w), dev(inf))
+    assert rel(r, P.PortOperator(m, k).apply(u, w, inf)) < APPLY_TOL
