@@ -1,0 +1,313 @@
+"""bench.py — convection-apply throughput on B200 (BASELINE.json metric).
+
+Workload (BASELINE cfg2, the config the headline metric is quoted on):
+256x256 squares -> 131,072 affine triangles, BDM_4 / V_h k=4, fp64, seeded
+divergence-free stream-function velocity (modes <= 16), inflow data from the
+same field.  One STEP = 100 forward-Euler explicit convection substeps,
+device-resident (hdgc_substeps), dt = 0.1 h / (k^2 max|u|).
+Metric: DOF/s = NT * nb * substeps / step time (one substep = one apply).
+
+Replicas only (SURVEY §8e / north star: one B200, no inter-GPU exchange):
+under torchrun every rank runs an independent replica; value = total DOF over
+all ranks / max-over-ranks time ("scaling": "weak").
+
+`--impl reference` times the reference-side CPU path instead: the reference
+ships no implementation of this operator, so it is the oracle's
+OpenMP C port (oracle/conv_port.c, "kind": "port") on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+K_ORDER = 4
+N_CELLS = 256
+MODES = 16
+SEED = 2
+NSUB = 100
+METRIC = "convection-apply DOF/s (fp64) at k=4"
+UNIT = "DOF/s"
+
+
+def pinned_work(k):
+    """SURVEY §8(d) pinned algorithmic work per element: (flops, bytes)."""
+    nb = (k + 1) * (k + 2)
+    nbs = nb // 2
+    nqv = [3, 7, 25, 36, 64, 81, 121, 144][k - 1]
+    nf = [3, 4, 6, 7, 9, 10, 12, 13][k - 1]
+    flops = 2 * (nqv * (2 * nb + 2 * nbs + 4 * nbs) + 3 * nf * ((k + 1) + 3 * nb))
+    return flops, 3 * nb * 8 + 16
+
+
+def fp64_peak():
+    """Measured FP64 peak (TFLOP/s) from tools/fp64_peak.cu on this pool
+    (profiles/fp64_peak_r01.json); MEASURED_PEAKS.json has no fp64 entry."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")) as fh:
+            d = json.loads(fh.readline())
+        return max(d["dfma_occ8_tflops"], d["dmma_m8n8k4_tflops"]), "profiles/fp64_peak_r01.json (measured DMMA m8n8k4)"
+    except Exception:
+        return 37.2, "nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (fallback)"
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "B200_PROFILING.md fallback"
+
+
+def workload():
+    from paper_1508_04245_b200 import fields as F
+    from paper_1508_04245_b200 import mesh as M
+    m = M.generate_structured((0.0, 0.0, 1.0, 1.0), N_CELLS, N_CELLS)
+    sf = F.StreamFunction(MODES, SEED)
+    u = F.interpolate_curl(m, K_ORDER, sf)
+    w = F.transfer_I_host(m, K_ORDER, u)
+    inflow = F.inflow_values(m, K_ORDER, sf)
+    dt = F.cfl_dt(m.h_min(), K_ORDER, F.max_speed_host(m, K_ORDER, u))
+    return m, u, w, inflow, dt
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if "--impl" not in sys.argv else "gloo")
+    return world, rank, local
+
+
+def run_reference(args, world, rank):
+    """CPU arm: the oracle's OpenMP C port on all host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from oracle import port as P
+    P.build()
+    m, u, w, inflow, dt = workload()
+    threads = os.cpu_count() or 1
+    op = P.PortOperator(m, K_ORDER, threads=threads)
+    nb = (K_ORDER + 1) * (K_ORDER + 2)
+    nsub = 1      # bounded sample: one substep over the full cfg2 mesh per step
+    for _ in range(args.warmup):
+        op.substeps(u, w, dt, nsub, inflow)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        op.substeps(u, w, dt, nsub, inflow)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = m.n_elements * nb * nsub / t
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: 256x256 structured, 131072 triangles, k=4, 1 forward-Euler substep per step "
+                               "(bounded CPU sample of the 100-substep GPU step)",
+                   "elements": m.n_elements, "k": K_ORDER, "substeps_per_step": nsub},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{nsub} substep(s) of cfg2 per step, {args.steps} steps"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def cpu_baseline_sample(m, u, w, inflow, dt, budget_s=10.0):
+    from oracle import port as P
+    P.build()
+    threads = os.cpu_count() or 1
+    op = P.PortOperator(m, K_ORDER, threads=threads)
+    nb = (K_ORDER + 1) * (K_ORDER + 2)
+    op.substeps(u, w, dt, 1, inflow)          # warm
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        op.substeps(u, w, dt, 1, inflow)
+        n += 1
+    t = time.perf_counter() - t0
+    return {"value": m.n_elements * nb * n / t, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{n} forward-Euler substeps of cfg2 (131072 tri, k=4) in {t:.1f} s, "
+                      f"oracle/conv_port.c OpenMP"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    from paper_1508_04245_b200.forms import ConvectionOperator
+
+    m, u, w, inflow, dt = workload()
+    op = ConvectionOperator(m, K_ORDER)
+    NT = m.n_elements
+    nb = (K_ORDER + 1) * (K_ORDER + 2)
+    ud = torch.from_numpy(u).cuda()
+    w0 = torch.from_numpy(w).cuda()
+    infd = torch.from_numpy(inflow).cuda()
+    wd = w0.clone()
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")   # > 126 MB L2
+
+    def step():
+        op.substeps(ud, wd, dt, NSUB, infd)
+
+    for _ in range(max(3, args.warmup)):
+        wd.copy_(w0)
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- timed region: K steps, L2 flushed before each (flush not timed)
+    clocks = ClockSampler(local) if rank == 0 else None
+    barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        wd.copy_(w0)
+        flush.fill_(float(i))
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop() if clocks else None
+    step_s = [a.elapsed_time(b) * 1e-3 for a, b in ev]
+    t_step = sum(step_s) / len(step_s)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t_step], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+    dofs_per_step = NT * nb * NSUB
+    value = world * dofs_per_step / t_step
+
+    # ---- per-launch duration of the substep kernel (L2 state as inside a step)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
+    wd.copy_(w0)
+    op.substeps(ud, wd, dt, 2, infd)
+    for a, b in kev:
+        a.record(stream)
+        op.substeps(ud, wd, dt, 1, infd)
+        b.record(stream)
+    torch.cuda.synchronize()
+    k_s = statistics.median(a.elapsed_time(b) * 1e-3 for a, b in kev)
+
+    # ---- e2e through the public API with pinned HOST buffers (H2D + 100 substeps + D2H)
+    uh = torch.from_numpy(u).pin_memory().numpy()
+    wh = torch.from_numpy(w).pin_memory().numpy()
+    ih = torch.from_numpy(inflow).pin_memory().numpy()
+    op.substeps_host(uh, wh, dt, NSUB, ih)
+    e2e_t = []
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.fill_(0.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        op.substeps_host(uh, wh, dt, NSUB, ih)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = statistics.median(e2e_t)
+
+    if rank != 0:
+        return
+    flops, byts = pinned_work(K_ORDER)
+    peak, peak_src = fp64_peak()
+    achieved = NT * flops / k_s / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_substep_r01.json")) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline_sample(m, u, w, inflow, dt)
+    hbm, hbm_src = hbm_peak()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: unit square 256x256 -> 131072 affine triangles, BDM_4/V_h k=4, "
+                               "seeded div-free stream function (modes<=16), 100 forward-Euler substeps per step",
+                   "elements": NT, "k": K_ORDER, "dofs_per_apply": NT * nb, "substeps_per_step": NSUB,
+                   "dt": dt, "l2": "flushed (512 MB write) before every timed step",
+                   "parallelism": f"replicas x{world}"},
+        "applies_per_s": world * NSUB / t_step,
+        "kernel_us_per_substep": k_s * 1e6,
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "algorithmic": f"pinned F(k=4)={flops} flop/element (SURVEY 8d) x {NT} elements per launch",
+                     "hbm_frac": NT * byts / k_s / 1e9 / hbm, "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src},
+        "cpu_baseline": cpu,
+        "e2e": {"value": world * dofs_per_step / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": int(u.nbytes + w.nbytes + inflow.nbytes),
+                "d2h_bytes_per_step": int(w.nbytes)},
+        "gpu_launches": args.steps * NSUB,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

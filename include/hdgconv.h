@@ -81,6 +81,17 @@ typedef struct {
   const double* fac_L;       /* (nf, nfd) facet normal-trace basis at facet points */
   const double* fac_D;       /* (nfaces, nf, nbs) Dubiner on each reference facet */
   const double* fac_len;     /* (nfaces) reference facet measures |e_hat| */
+  /* sum-factorisation tables on the collapsed volume rule (2D, k >= 3; else 0/NULL):
+   * D_ij(xi_a, y_b) = A_i(a) B_ij(b); see basis.collapsed_tables */
+  int32_t col_n;             /* points per direction, (3k+1)/2 */
+  const double* col_A;       /* (n, k+1) P_i(2 xi_a - 1) */
+  const double* col_Ad;      /* (n, k+1) d/dxi */
+  const double* col_B;       /* (n, nbs) c_ij (1-y_b)^i P_j^(2i+1,0)(2 y_b - 1) */
+  const double* col_Bd;      /* (n, nbs) d/dy at fixed xi */
+  const double* col_xi;      /* (n) */
+  const double* col_wa;      /* (n) */
+  const double* col_wy;      /* (n) */
+  const double* col_inv1my;  /* (n) 1/(1-y_b) */
 } hdgc_tables_desc;
 
 typedef struct {

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhdgconv.so")
+LIB_PATH = os.environ.get("HDGC_LIB", os.path.join(HERE, "libhdgconv.so"))
 
 # exported symbols, in include/hdgconv.h order
 SYMBOLS = (
@@ -37,6 +37,9 @@ class TablesDesc(C.Structure):
         ("coef", C.c_void_p), ("div_modal", C.c_void_p), ("vol_w", C.c_void_p), ("vol_D", C.c_void_p),
         ("vol_G", C.c_void_p), ("fac_w", C.c_void_p), ("fac_L", C.c_void_p),
         ("fac_D", C.c_void_p), ("fac_len", C.c_void_p),
+        ("col_n", C.c_int32), ("col_A", C.c_void_p), ("col_Ad", C.c_void_p), ("col_B", C.c_void_p),
+        ("col_Bd", C.c_void_p), ("col_xi", C.c_void_p), ("col_wa", C.c_void_p), ("col_wy", C.c_void_p),
+        ("col_inv1my", C.c_void_p),
     ]
 
 

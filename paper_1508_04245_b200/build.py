@@ -1,12 +1,16 @@
 """In-tree build of the CUDA library (sm_100a) — ``python -m paper_1508_04245_b200.build``.
 
-Produces ``paper_1508_04245_b200/libhdgconv.so`` with
-``nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -shared``.
-The .so is git-ignored but travels to the GPU box with the repo snapshot.
+Produces ``paper_1508_04245_b200/libhdgconv.so``.  Every translation unit
+(hdgconv.cu: C ABI + setup kernels; order_k<K>.cu: the kernels of order K)
+is compiled in parallel with
+``nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -Xptxas -v -c``
+and linked with ``nvcc -shared``.  Objects are cached by source mtime.  The
+.so is git-ignored but travels to the GPU box with the repo snapshot.
 """
 
 from __future__ import annotations
 
+import concurrent.futures as cf
 import glob
 import os
 import shutil
@@ -16,8 +20,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "_obj")
 OUT = os.path.join(HERE, "libhdgconv.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
 def nvcc() -> str:
@@ -27,32 +33,54 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
-                  + [os.path.join(ROOT, "include", "hdgconv.h")])
+def headers():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "hdgconv.h")])
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(OUT):
-        return False
-    t = os.path.getmtime(OUT)
-    return all(os.path.getmtime(s) <= t for s in sources())
+def units():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _compile(src):
+    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+    if not _stale(obj, [src] + headers()):
+        return obj, None
+    cmd = [nvcc(), *ARCH, *FLAGS, "-c", "-o", obj + ".tmp", src]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed on {src}:\n{res.stdout}{res.stderr}")
+    os.replace(obj + ".tmp", obj)
+    with open(obj[:-2] + ".ptxas.log", "w") as fh:
+        fh.write(res.stderr)
+    return obj, res.stderr
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return OUT
-    cmd = [nvcc(), *ARCH, "-lineinfo", "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v", "-o", OUT + ".tmp", os.path.join(CSRC, "hdgconv.cu")]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libhdgconv.so")
-    with open(os.path.join(HERE, "build_ptxas.log"), "w") as fh:
-        fh.write(res.stderr)
-    os.replace(OUT + ".tmp", OUT)
+    os.makedirs(OBJ, exist_ok=True)
+    if force:
+        for f in glob.glob(os.path.join(OBJ, "*.o")):
+            os.remove(f)
+    srcs = units()
+    with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(_compile, srcs))
+    objs = [o for o, _ in results]
+    if _stale(OUT, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", OUT + ".tmp", *objs]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"link failed:\n{res.stdout}{res.stderr}")
+        os.replace(OUT + ".tmp", OUT)
     if verbose:
-        print(res.stderr)
+        for _, log in results:
+            if log:
+                print(log)
     return OUT
 
 

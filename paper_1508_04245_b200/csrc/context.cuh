@@ -1,0 +1,67 @@
+// context.cuh — device context, error plumbing and the per-order entry
+// points shared by hdgconv.cu (C ABI) and the per-order translation units
+// order_k*.cu (one per k, compiled in parallel).
+#pragma once
+#include "../../include/hdgconv.h"
+
+#include <cstdint>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+int hdgc_set_err(int code, const char* fmt, ...);
+
+#define CUDA_TRY(x)                                                                           \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess)                                                                    \
+      return hdgc_set_err(HDGC_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, \
+                          __LINE__);                                                          \
+  } while (0)
+
+struct hdgc_ctx {
+  int dim = 2, k = 0, nb = 0, nbs = 0, nqv = 0, nf = 0;
+  int nt = 0, nf_facets = 0, nbf = 0, nv = 0;
+  double* d_tab = nullptr;      // packed tables (Dims<K> layout)
+  int32_t* d_code = nullptr;    // (NT, 3) neighbour codes
+  double* d_piola = nullptr;    // (4, NT) J/detJ
+  double* d_minv = nullptr;     // (NT,) 2/detJ
+  double* d_scratch = nullptr;  // (NT, nb) ping-pong / I u
+  double* d_prep = nullptr;     // (NT, PREP) frozen-velocity data (sum-factorised variant)
+  double* d_modal = nullptr;    // (NT, nb + nbs(k-1)) modal u_hat | div u_hat
+  double* d_scratch2 = nullptr; // (NT, nb) r_V for apply_w (lazily allocated)
+  double* d_ftab = nullptr;     // facet tables fw | fD (sum-factorised variant)
+  // host-variant staging (lazily allocated)
+  double* d_hu = nullptr;
+  double* d_hw = nullptr;
+  double* d_hr = nullptr;
+  double* d_hin = nullptr;
+  int64_t bytes = 0;
+  int variant = 0;              // 0: thread-per-element (k <= 2), 1: sum-factorised (k >= 3)
+};
+
+int hdgc_dev_alloc(hdgc_ctx* c, void** p, size_t bytes);
+
+namespace hdgc {
+// per-order operations, explicitly instantiated in order_k<K>.cu
+template <int K> int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w,
+                                 const double* inflow, double* out, double dt, cudaStream_t st);
+template <int K> int launch_transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st);
+template <int K> int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st);
+template <int K> int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st);
+template <int K> int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out,
+                             double dt, cudaStream_t st);
+template <int K> int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& packed);
+
+#define HDGC_DECLARE_ORDER(K)                                                                      \
+  extern template int launch_elem<K>(hdgc_ctx*, int, const double*, const double*, const double*,  \
+                                     double*, double, cudaStream_t);                               \
+  extern template int launch_transfer<K>(hdgc_ctx*, int, const double*, double*, cudaStream_t);    \
+  extern template int launch_maxspeed<K>(hdgc_ctx*, const double*, double*, cudaStream_t);         \
+  extern template int sf_prep<K>(hdgc_ctx*, const double*, cudaStream_t);                          \
+  extern template int sf_main<K>(hdgc_ctx*, int, const double*, const double*, double*, double,    \
+                                 cudaStream_t);                                                    \
+  extern template int sf_setup<K>(hdgc_ctx*, const hdgc_tables_desc*, const std::vector<double>&);
+}  // namespace hdgc

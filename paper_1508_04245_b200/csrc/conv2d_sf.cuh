@@ -1,0 +1,519 @@
+// Variant "sf": sum-factorised flux-difference apply for k >= 3 on the
+// collapsed (Duffy) volume rule, n = (3k+1)/2 points per direction.
+//
+// The convecting velocity is frozen over an apply and over a whole substep
+// batch, so everything that depends on u alone is
+// evaluated once per batch (rowmat2d_kernel + prep_points2d_kernel) into a
+// per-element "prep row":
+//   alpha(p) = w_p (u0 + xi_p u1) / (1 - y_p),   beta(p) = w_p u1,
+//   gamma(p) = w_p div u_hat                      at the n^2 volume points,
+//   s_e(q)   = w_q F_e(t_q) if F_e(t_q) < 0 else 0   (inflow points, 3 nf)
+// (u_hat = Piola-free reference velocity, F = u.n ds/dt from the edge dofs,
+// SURVEY.md A.3/A.4).  This is quadrature-point data, not an assembled
+// matrix.  The per-substep kernel then only moves w:
+//
+//   r_c[ij] = sum_b B_ij(b) sum_a A_i(a) g_c(a,b)
+//   g_c     = alpha d_xi w_c + beta d_y|xi w_c + gamma w_c
+//           ( = w_p (u.grad w_c + w_c div u) at the point, flux-difference
+//             form, see conv2d_thread.cuh )
+//   w_c and its derivatives at the points by sum factorisation: per row b
+//   H_i = sum_j w_c,ij B_ij(b), H'_i = sum_j w_c,ij dB_ij/dy(b), then
+//   w = sum_i A_i(a) H_i, d_xi w = sum_i A'_i(a) H_i, d_y|xi w = sum_i A_i(a) H'_i.
+//   + sum_e sum_{q inflow} s_e(q) (w_ext - w_own)_c(q) D_m(x_e(q))
+//
+// FMA per element (k=4): volume 2 x 6 x (30 + 6 x 23 + 15) = 2196 plus the
+// inflow facet points, against 7395 for the pinned direct form.
+//
+// Work split: one CTA = EPB elements, two threads per element (one per output
+// component c); prep rows and w (interleaved (m, c)) staged in shared memory;
+// A/A'/B/B' tables in the constant bank (uniform operands).
+#pragma once
+#include "common.cuh"
+
+namespace hdgc {
+
+__host__ __device__ constexpr int midx(int i, int j) { return (i + j) * (i + j + 1) / 2 + j; }
+
+template <int K>
+struct SF {
+  static constexpr int N = (3 * K + 1) / 2;   // collapsed points per direction
+  static constexpr int NQ = N * N;
+  static constexpr int NE = K + 1;
+  static constexpr int NBS = (K + 1) * (K + 2) / 2;
+  static constexpr int NB = 2 * NBS;
+  static constexpr int NBS1 = K * (K + 1) / 2;
+  static constexpr int NF = (3 * K + 3) / 2;
+  // constant-bank table layout (doubles)
+  static constexpr int C_A = 0;                    // [N][K+1]  P_i(2 xi_a - 1)
+  static constexpr int C_AD = C_A + N * NE;        // [N][K+1]  d/dxi
+  static constexpr int C_B = C_AD + N * NE;        // [N][NBS]  c_ij (1-y)^i P_j^(2i+1,0)(2y-1)
+  static constexpr int C_BD = C_B + N * NBS;       // [N][NBS]  d/dy at fixed xi
+  static constexpr int C_PA = C_BD + N * NBS;      // [NQ] w_p / (1 - y_p)
+  static constexpr int C_PB = C_PA + NQ;           // [NQ] w_p xi_p / (1 - y_p)
+  static constexpr int C_PW = C_PB + NQ;           // [NQ] w_p
+  static constexpr int C_TOTAL = C_PW + NQ;
+  // prep row: alpha | beta | gamma | s, padded to PREP_PAD doubles (16-B rows for
+  // the bulk copy; PREP_PAD = 2 mod 4 spreads the per-element rows over the banks)
+  static constexpr int P_AL = 0;
+  static constexpr int P_BE = NQ;
+  static constexpr int P_GA = 2 * NQ;
+  static constexpr int P_S = 3 * NQ;
+  static constexpr int PREP = 3 * NQ + 3 * NF;
+  static constexpr int PREP_PAD = PREP + ((2 - PREP % 4) + 4) % 4;
+  static constexpr int EPB = 16;                    // elements per CTA
+  static constexpr int THREADS = 2 * EPB;
+  // smem (doubles): mbarrier | prep tile [EPB][PREP_PAD] | w tile [EPB][NB] |
+  //                 halo [THREADS][NBS] | fD [3][NF][NBS]
+  static constexpr int SM_BAR = 0;
+  static constexpr int SM_PREP = 2;
+  static constexpr int SM_W = SM_PREP + EPB * PREP_PAD;
+  static constexpr int SM_HALO = SM_W + EPB * NB;
+  static constexpr int SM_FD = SM_HALO + THREADS * NBS + ((THREADS * NBS) & 1);
+  static constexpr int TAB = 3 * NF * NBS;
+  static constexpr int TAB_PAD = TAB + (TAB & 1);   // 16-B multiple for the bulk copy
+  static constexpr int SMEM_DOUBLES = SM_FD + TAB_PAD;
+};
+
+// The constant-bank tables of the order compiled in this translation unit
+// (order_k<K>.cu defines HDGC_ORDER before including the kernels).
+#ifndef HDGC_ORDER
+#error "define HDGC_ORDER (the order k of this translation unit) before including conv2d_sf.cuh"
+#endif
+#if HDGC_ORDER >= 3
+__constant__ double c_sf[SF<HDGC_ORDER>::C_TOTAL];
+__constant__ double c_fd[SF<HDGC_ORDER>::TAB];   // Dubiner traces fD[3][NF][NBS]
+// fused prep (k <= 6): [coef ; divm] (NB + NBS1 rows x NB) | fL (NF x NE) | fw (NF) | flen (3)
+#define HDGC_CM_FUSED (HDGC_ORDER <= 6)
+#if HDGC_CM_FUSED
+__constant__ double c_cm[(SF<HDGC_ORDER>::NB + SF<HDGC_ORDER>::NBS1) * SF<HDGC_ORDER>::NB +
+                         SF<HDGC_ORDER>::NF * SF<HDGC_ORDER>::NE + SF<HDGC_ORDER>::NF + 3];
+#else
+__constant__ double c_cm[1];
+#endif
+#else
+__constant__ double c_sf[1];
+__constant__ double c_fd[1];
+#define HDGC_CM_FUSED 0
+__constant__ double c_cm[1];
+#endif
+
+template <int K> __device__ __forceinline__ const double* sf_tab() {
+  static_assert(K == HDGC_ORDER, "sum-factorisation tables are per translation unit");
+  return c_sf;
+}
+template <int K> __device__ __forceinline__ const double* fd_tab() {
+  static_assert(K == HDGC_ORDER, "facet tables are per translation unit");
+  return c_fd;
+}
+
+// ---------------------------------------------------------------------------
+// fused prep (k <= 6), one thread per element: modal u_hat = coef u and
+// div = divm u with the matrices as constant-bank operands, then alpha/beta/
+// gamma at the n x n points by sum factorisation of the velocity (per row b:
+// H_i = sum_j u_hat_ij B_ij(b), then sum_i A_i(a) H_i), and the inflow weights.
+template <int K>
+__global__ void __launch_bounds__(128)
+prep_fused2d_kernel(const double* __restrict__ u, int nt, double* __restrict__ prep) {
+  using F = SF<K>;
+  constexpr int N = F::N, NE = F::NE, NBS = F::NBS, NB = F::NB, NBS1 = F::NBS1, NF = F::NF;
+  constexpr int O_FL = (NB + NBS1) * NB, O_FW = O_FL + NF * NE, O_FLEN = O_FW + NF;
+  const double* CM = c_cm;
+  const double* C = sf_tab<K>();
+  const int T = blockIdx.x * blockDim.x + threadIdx.x;
+  if (T >= nt) return;
+  double* out = prep + (size_t)T * F::PREP_PAD;
+  double uh[NB], dv[NBS1 > 0 ? NBS1 : 1];
+  {
+    double x[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) x[j] = __ldg(u + (size_t)T * NB + j);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+#pragma unroll
+      for (int q = 0; q < NF; ++q) {
+        double a = 0.0;
+#pragma unroll
+        for (int l = 0; l < NE; ++l) a = fma(x[e * NE + l], CM[O_FL + q * NE + l], a);
+        const double Fq = a * CM[O_FLEN + e];
+        out[F::P_S + e * NF + q] = Fq < 0.0 ? CM[O_FW + q] * Fq : 0.0;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      double a = 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) a = fma(CM[i * NB + j], x[j], a);
+      uh[i] = a;
+    }
+#pragma unroll
+    for (int i = 0; i < NBS1; ++i) {
+      double a = 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) a = fma(CM[(NB + i) * NB + j], x[j], a);
+      dv[i] = a;
+    }
+  }
+#pragma unroll 1
+  for (int b = 0; b < N; ++b) {
+    const double* Bb = C + F::C_B + b * NBS;
+    double H0[NE], H1[NE], Hd[NE];
+#pragma unroll
+    for (int i = 0; i <= K; ++i) {
+      double s0 = 0.0, s1 = 0.0, sd = 0.0;
+#pragma unroll
+      for (int j = 0; j <= K - i; ++j) {
+        const int m = midx(i, j);
+        s0 = fma(uh[m], Bb[m], s0);
+        s1 = fma(uh[NBS + m], Bb[m], s1);
+        if (i + j < K) sd = fma(dv[m], Bb[m], sd);
+      }
+      H0[i] = s0; H1[i] = s1; Hd[i] = sd;
+    }
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      double u0 = 0.0, u1 = 0.0, dq = 0.0;
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        const double Ai = C[F::C_A + a * NE + i];
+        u0 = fma(Ai, H0[i], u0);
+        u1 = fma(Ai, H1[i], u1);
+        if (i < K) dq = fma(Ai, Hd[i], dq);
+      }
+      const int p = b * N + a;
+      out[F::P_AL + p] = fma(C[F::C_PA + p], u0, C[F::C_PB + p] * u1);
+      out[F::P_BE + p] = C[F::C_PW + p] * u1;
+      out[F::P_GA + p] = C[F::C_PW + p] * dq;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// prep, stage 2 (stage 1 = modal u_hat | div, rowmat2d_kernel): one thread
+// per (element, slot), slot < NQ: alpha/beta/gamma at volume point p;
+// NQ <= slot < NQ + 3 NF: inflow weight s_e(q) from the raw edge dofs.
+template <int K>
+__global__ void __launch_bounds__(256)
+prep_points2d_kernel(const double* __restrict__ tab, const double* __restrict__ u,
+                     const double* __restrict__ modal, int nt, double* __restrict__ prep) {
+  using D = Dims<K>;
+  using F = SF<K>;
+  constexpr int NB = D::NB, NBS = D::NBS, NBS1 = D::NBS1, NE = D::NE, NF = D::NF, NQ = F::NQ;
+  constexpr int R = NQ + 3 * NF;            // slots per element (pad slots untouched)
+  constexpr int MR = NB + NBS1;             // modal row length
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)nt * R) return;
+  const int T = (int)(gid / R);
+  const int slot = (int)(gid - (long long)T * R);
+  const double* C = sf_tab<K>();
+  double* out = prep + (size_t)T * F::PREP_PAD;
+  if (slot < NQ) {
+    const double* Dp = tab + D::OFF_VD + slot * NBS;
+    const double* mr = modal + (size_t)T * MR;
+    double u0 = 0.0, u1 = 0.0, dq = 0.0;
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) {
+      const double d = __ldg(Dp + m);
+      u0 = fma(__ldg(mr + m), d, u0);
+      u1 = fma(__ldg(mr + NBS + m), d, u1);
+      if (m < NBS1) dq = fma(__ldg(mr + NB + m), d, dq);
+    }
+    out[F::P_AL + slot] = fma(C[F::C_PA + slot], u0, C[F::C_PB + slot] * u1);
+    out[F::P_BE + slot] = C[F::C_PW + slot] * u1;
+    out[F::P_GA + slot] = C[F::C_PW + slot] * dq;
+  } else {
+    const int eq = slot - NQ, e = eq / NF, q = eq - e * NF;
+    double a = 0.0;
+#pragma unroll
+    for (int l = 0; l < NE; ++l) a = fma(__ldg(u + (size_t)T * NB + e * NE + l), __ldg(tab + D::OFF_FL + q * NE + l), a);
+    const double Fq = a * __ldg(tab + D::OFF_FLEN + e);
+    out[F::P_S + eq] = Fq < 0.0 ? __ldg(tab + D::OFF_FW + q) * Fq : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-apply / per-substep kernel
+struct SFParams {
+  const double* __restrict__ prep;    // (NT, PREP_PAD)
+  const double* __restrict__ w;       // (NT, NB)
+  const double* __restrict__ inflow;  // (NBF, NF, 2) or nullptr
+  const int32_t* __restrict__ code;   // (NT, 3)
+  const double* __restrict__ minv;    // (NT,)
+  const double* __restrict__ ftab;    // fD[3][NF][NBS] (global copy)
+  double* __restrict__ out;           // (NT, NB)
+  double dt;
+  int nt;
+};
+
+// --- TMA bulk copies + mbarrier (sm_90+ PTX; SASS UBLKCP / SYNCS)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(SF<K>::THREADS)
+conv2d_sf_kernel(SFParams p) {
+  using F = SF<K>;
+  constexpr int N = F::N, NE = F::NE, NBS = F::NBS, NB = F::NB, NF = F::NF, EPB = F::EPB;
+  extern __shared__ __align__(128) double sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + F::SM_BAR);
+  double* s_prep = sm + F::SM_PREP;        // [EPB][PREP_PAD]
+  double* s_w = sm + F::SM_W;              // [EPB][NB]  (c-major, as in global)
+  double* s_halo = sm + F::SM_HALO;        // [THREADS][NBS]
+  double* s_fD = sm + F::SM_FD;            // [3][NF][NBS]
+  const double* C = sf_tab<K>();
+
+  const int T0 = blockIdx.x * EPB;
+  const int nel = min(EPB, p.nt - T0);
+  // ---- stage the tile with two bulk copies (one mbarrier phase)
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t bp = (uint32_t)(nel * F::PREP_PAD * sizeof(double));
+    const uint32_t bw = (uint32_t)(nel * NB * sizeof(double));
+    const uint32_t bt = (uint32_t)(F::TAB_PAD * sizeof(double));
+    mbar_arrive_expect_tx(bar, bp + bw + bt);
+    bulk_g2s(s_prep, p.prep + (size_t)T0 * F::PREP_PAD, bp, bar);
+    bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
+    bulk_g2s(s_fD, p.ftab, bt, bar);
+  }
+
+  const int le = threadIdx.x >> 1;
+  const int c = threadIdx.x & 1;
+  const bool active = le < nel;
+  const int T = T0 + (active ? le : 0);
+  int codes[3];
+#pragma unroll
+  for (int ed = 0; ed < 3; ++ed) codes[ed] = active ? __ldg(p.code + (size_t)T * 3 + ed) : -1;
+  const double sc = MODE == MODE_SUBSTEP && active ? p.dt * __ldg(p.minv + T) : 0.0;
+  mbar_wait(bar, 0);
+
+  const double* row = s_prep + (active ? le : 0) * F::PREP_PAD;
+  const double* wc = s_w + (active ? le : 0) * NB + c * NBS;      // w_c[m]
+  double* halo = s_halo + threadIdx.x * NBS;
+
+  // ---- prefetch (cp.async) the first out-of-tile inflow neighbour trace data
+  int halo_edge = -1;
+  if (active) {
+#pragma unroll
+    for (int ed = 0; ed < 3; ++ed) {
+      const int code = codes[ed];
+      if (code < 0 || halo_edge >= 0) continue;
+      const int nbT = code >> 2;
+      if (nbT >= T0 && nbT < T0 + nel) continue;
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < NF; ++q) any |= row[F::P_S + ed * NF + q] != 0.0;
+      if (!any) continue;
+      halo_edge = ed;
+      const double* g = p.w + (size_t)nbT * NB + c * NBS;
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) cp_async8(halo + m, g + m);
+    }
+  }
+
+  double r[NBS], wo[NBS];
+#pragma unroll
+  for (int m = 0; m < NBS; ++m) {
+    r[m] = 0.0;
+    wo[m] = wc[m];      // own w_c in registers for the volume and facet terms
+  }
+
+  // ---- volume, sum-factorised over rows b of the collapsed rule
+#ifdef HDGC_ROW_UNROLL
+  constexpr int ROW_UNROLL = HDGC_ROW_UNROLL;
+#else
+  constexpr int ROW_UNROLL = 1;   // rolled: the unrolled body overflows the i-cache (ncu: no_instruction stalls)
+#endif
+#pragma unroll ROW_UNROLL
+  for (int b = 0; b < N; ++b) {
+    const double* Bb = C + F::C_B + b * NBS;
+    const double* Bdb = C + F::C_BD + b * NBS;
+    double Hw[NE], Hwd[NE];
+#pragma unroll
+    for (int i = 0; i <= K; ++i) {
+      double sw = 0.0, swd = 0.0;
+#pragma unroll
+      for (int j = 0; j <= K - i; ++j) {
+        const int m = midx(i, j);
+        const double wv = wo[m];
+        sw = fma(wv, Bb[m], sw);
+        swd = fma(wv, Bdb[m], swd);
+      }
+      Hw[i] = sw;
+      Hwd[i] = swd;
+    }
+    const double* al = row + F::P_AL + b * N;
+    const double* be = row + F::P_BE + b * N;
+    const double* ga = row + F::P_GA + b * N;
+    double Kc[NE];
+#pragma unroll
+    for (int i = 0; i <= K; ++i) Kc[i] = 0.0;
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      double wv = 0.0, wxi = 0.0, wyy = 0.0;
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        const double Ai = C[F::C_A + a * NE + i];
+        wv = fma(Ai, Hw[i], wv);
+        wxi = fma(C[F::C_AD + a * NE + i], Hw[i], wxi);
+        wyy = fma(Ai, Hwd[i], wyy);
+      }
+      const double g = fma(al[a], wxi, fma(be[a], wyy, ga[a] * wv));
+#pragma unroll
+      for (int i = 0; i <= K; ++i) Kc[i] = fma(g, C[F::C_A + a * NE + i], Kc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i <= K; ++i) {
+#pragma unroll
+      for (int j = 0; j <= K - i; ++j) {
+        const int m = midx(i, j);
+        r[m] = fma(Kc[i], Bb[m], r[m]);
+      }
+    }
+  }
+
+  // ---- facets: upwind jump at inflow points only (s != 0).  Own-edge traces and
+  //      the test use compile-time constant-bank operands (ed, q unrolled); the
+  //      neighbour's edge e2 varies per thread, so its table is read from smem.
+  if (halo_edge >= 0) cp_async_wait_all();
+  const double* FD = fd_tab<K>();
+  if (active) {
+#pragma unroll
+    for (int ed = 0; ed < 3; ++ed) {
+      const double* se = row + F::P_S + ed * NF;
+      double sv[NF];
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < NF; ++q) {
+        sv[q] = se[q];
+        any |= sv[q] != 0.0;
+      }
+      if (!any) continue;
+      const int code = codes[ed];
+      double wn[NBS];
+      const double* infl = nullptr;
+      int e2 = 0;
+      if (code >= 0) {
+        const int nbT = code >> 2;
+        e2 = code & 3;
+        const double* src = (nbT >= T0 && nbT < T0 + nel) ? s_w + (nbT - T0) * NB + c * NBS
+                            : (ed == halo_edge) ? halo : nullptr;
+        if (src != nullptr) {
+#pragma unroll
+          for (int m = 0; m < NBS; ++m) wn[m] = src[m];
+        } else {
+          const double* g = p.w + (size_t)nbT * NB + c * NBS;
+#pragma unroll
+          for (int m = 0; m < NBS; ++m) wn[m] = __ldg(g + m);
+        }
+      } else if (p.inflow != nullptr) {
+        infl = p.inflow + (size_t)(-1 - code) * NF * 2 + c;
+      } else {
+        continue;   // boundary without inflow data: exterior = own trace
+      }
+      // all NF points of the edge at once: NF independent accumulation chains;
+      // outflow points carry sv[q] = 0 and contribute nothing
+      double own[NF], ext[NF];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) own[q] = 0.0;
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) {
+#pragma unroll
+        for (int q = 0; q < NF; ++q) own[q] = fma(wo[m], FD[(ed * NF + q) * NBS + m], own[q]);
+      }
+      if (code >= 0) {
+        const double* Dn = s_fD + e2 * NF * NBS;   // neighbour edge, reversed points
+#pragma unroll
+        for (int q = 0; q < NF; ++q) ext[q] = 0.0;
+#pragma unroll
+        for (int m = 0; m < NBS; ++m) {
+#pragma unroll
+          for (int q = 0; q < NF; ++q) ext[q] = fma(wn[m], Dn[(NF - 1 - q) * NBS + m], ext[q]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < NF; ++q) ext[q] = sv[q] != 0.0 ? __ldg(infl + 2 * q) : own[q];
+      }
+#pragma unroll
+      for (int q = 0; q < NF; ++q) own[q] = sv[q] * (ext[q] - own[q]);
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) {
+        double acc = r[m];
+#pragma unroll
+        for (int q = 0; q < NF; ++q) acc = fma(own[q], FD[(ed * NF + q) * NBS + m], acc);
+        r[m] = acc;
+      }
+    }
+  }
+
+  // ---- epilogue: outputs into the w tile (in-tile neighbour reads are done),
+  //      then one bulk store of the tile
+  __syncthreads();
+  if (active) {
+    double* wo = s_w + le * NB + c * NBS;
+    if (MODE == MODE_SUBSTEP) {
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) wo[m] = fma(-sc, r[m], wo[m]);
+    } else {
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) wo[m] = r[m];
+    }
+  }
+  fence_proxy_async();   // generic-proxy smem writes -> visible to the bulk copy
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bulk_s2g(p.out + (size_t)T0 * NB, s_w, (uint32_t)(nel * NB * sizeof(double)));
+    bulk_wait_read();
+  }
+}
+
+}  // namespace hdgc

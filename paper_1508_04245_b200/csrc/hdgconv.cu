@@ -9,7 +9,7 @@
 #include <vector>
 
 #include "common.cuh"
-#include "conv2d_thread.cuh"
+#include "context.cuh"
 
 using namespace hdgc;
 
@@ -18,7 +18,7 @@ using namespace hdgc;
 
 static thread_local std::string g_err;
 
-static int set_err(int code, const char* fmt, ...) {
+int hdgc_set_err(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -28,37 +28,13 @@ static int set_err(int code, const char* fmt, ...) {
   return code;
 }
 
-#define CUDA_TRY(x)                                                                      \
-  do {                                                                                   \
-    cudaError_t e_ = (x);                                                                \
-    if (e_ != cudaSuccess)                                                               \
-      return set_err(HDGC_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, \
-                     __LINE__);                                                          \
-  } while (0)
 
 // ---------------------------------------------------------------------------
 // context
 
-struct hdgc_ctx {
-  int dim = 2, k = 0, nb = 0, nbs = 0, nqv = 0, nf = 0;
-  int nt = 0, nf_facets = 0, nbf = 0, nv = 0;
-  double* d_tab = nullptr;      // packed tables (Dims<K> layout)
-  int32_t* d_code = nullptr;    // (NT, 3) neighbour codes
-  double* d_piola = nullptr;    // (4, NT) J/detJ
-  double* d_minv = nullptr;     // (NT,) 2/detJ
-  double* d_scratch = nullptr;  // (NT, nb) ping-pong / I u
-  // host-variant staging (lazily allocated)
-  double* d_hu = nullptr;
-  double* d_hw = nullptr;
-  double* d_hr = nullptr;
-  double* d_hin = nullptr;
-  int64_t bytes = 0;
-  int variant = 0;
-};
-
-static int dev_alloc(hdgc_ctx* c, void** p, size_t bytes) {
+int hdgc_dev_alloc(hdgc_ctx* c, void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes);
-  if (e != cudaSuccess) return set_err(HDGC_ENOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+  if (e != cudaSuccess) return hdgc_set_err(HDGC_ENOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
   c->bytes += (int64_t)bytes;
   return HDGC_OK;
 }
@@ -136,149 +112,16 @@ __global__ void codes_kernel(const int64_t* __restrict__ fe, const int64_t* __re
   }
 }
 
-// ---------------------------------------------------------------------------
-// transfer kernels:  I (BDM -> V_h)  and  I^T (V_h functionals -> BDM-test)
-
-template <int K, bool TRANSPOSE>
-__global__ void __launch_bounds__(128)
-transfer2d_kernel(const double* __restrict__ tab, const double* __restrict__ piola, int nt,
-                  const double* __restrict__ in, double* __restrict__ out) {
-  using D = Dims<K>;
-  constexpr int NB = D::NB, NBS = D::NBS;
-  const int T = blockIdx.x * blockDim.x + threadIdx.x;
-  if (T >= nt) return;
-  const double* coef = tab + D::OFF_COEF;
-  const double P00 = piola[T], P01 = piola[(size_t)nt + T];
-  const double P10 = piola[2 * (size_t)nt + T], P11 = piola[3 * (size_t)nt + T];
-  double x[NB];
-#pragma unroll
-  for (int j = 0; j < NB; ++j) x[j] = in[(size_t)T * NB + j];
-  if (!TRANSPOSE) {
-    // w[c,m] = sum_d P[c][d] (coef u)[d,m]
-    double uh[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      double a = 0.0;
-#pragma unroll
-      for (int j = 0; j < NB; ++j) a = fma(__ldg(coef + i * NB + j), x[j], a);
-      uh[i] = a;
-    }
-#pragma unroll
-    for (int m = 0; m < NBS; ++m) {
-      out[(size_t)T * NB + m] = fma(P00, uh[m], P01 * uh[NBS + m]);
-      out[(size_t)T * NB + NBS + m] = fma(P10, uh[m], P11 * uh[NBS + m]);
-    }
-  } else {
-    double s[NB];
-#pragma unroll
-    for (int m = 0; m < NBS; ++m) {
-      s[m] = fma(P00, x[m], P10 * x[NBS + m]);
-      s[NBS + m] = fma(P01, x[m], P11 * x[NBS + m]);
-    }
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      double a = 0.0;
-#pragma unroll
-      for (int i = 0; i < NB; ++i) a = fma(__ldg(coef + i * NB + j), s[i], a);
-      out[(size_t)T * NB + j] = a;
-    }
-  }
-}
-
-// max |J u_hat / detJ| over elements x volume points (positive doubles order as uint64)
-template <int K>
-__global__ void __launch_bounds__(128)
-maxspeed2d_kernel(const double* __restrict__ tab, const double* __restrict__ piola, int nt,
-                  const double* __restrict__ u, unsigned long long* __restrict__ out) {
-  using D = Dims<K>;
-  constexpr int NB = D::NB, NBS = D::NBS;
-  const int T = blockIdx.x * blockDim.x + threadIdx.x;
-  double best = 0.0;
-  if (T < nt) {
-    const double* coef = tab + D::OFF_COEF;
-    const double* vD = tab + D::OFF_VD;
-    double uh[NB];
-    {
-      double x[NB];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) x[j] = u[(size_t)T * NB + j];
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        double a = 0.0;
-#pragma unroll
-        for (int j = 0; j < NB; ++j) a = fma(__ldg(coef + i * NB + j), x[j], a);
-        uh[i] = a;
-      }
-    }
-    const double P00 = piola[T], P01 = piola[(size_t)nt + T];
-    const double P10 = piola[2 * (size_t)nt + T], P11 = piola[3 * (size_t)nt + T];
-    for (int q = 0; q < D::NQV; ++q) {
-      double a = 0.0, b = 0.0;
-#pragma unroll
-      for (int m = 0; m < NBS; ++m) {
-        const double d = __ldg(vD + q * NBS + m);
-        a = fma(uh[m], d, a);
-        b = fma(uh[NBS + m], d, b);
-      }
-      const double x = fma(P00, a, P01 * b), y = fma(P10, a, P11 * b);
-      best = fmax(best, sqrt(fma(x, x, y * y)));
-    }
-  }
-  for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
-}
-
-// ---------------------------------------------------------------------------
-// dispatch
-
-template <int K>
-static int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow,
-                       double* out, double dt, cudaStream_t st) {
-  ElemParams p;
-  p.tab = c->d_tab;
-  p.u = u;
-  p.w = w;
-  p.inflow = inflow;
-  p.code = c->d_code;
-  p.piola = c->d_piola;
-  p.minv = c->d_minv;
-  p.out = out;
-  p.dt = dt;
-  p.nt = c->nt;
-  const int threads = 128;
-  const int blocks = (c->nt + threads - 1) / threads;
-  const int smem = thread_smem_bytes<K>();
-  auto launch = [&](auto kern) -> int {
-    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<blocks, threads, smem, st>>>(p);
-    CUDA_TRY(cudaGetLastError());
-    return HDGC_OK;
-  };
-  switch (mode) {
-    case MODE_APPLY: return launch(conv2d_thread_kernel<K, MODE_APPLY>);
-    case MODE_SUBSTEP: return launch(conv2d_thread_kernel<K, MODE_SUBSTEP>);
-    default: return launch(conv2d_thread_kernel<K, MODE_APPLY_IT>);
-  }
-}
-
-template <int K>
-static int launch_transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st) {
-  const int threads = 128, blocks = (c->nt + threads - 1) / threads;
-  if (dir == 0) transfer2d_kernel<K, false><<<blocks, threads, 0, st>>>(c->d_tab, c->d_piola, c->nt, in, out);
-  else transfer2d_kernel<K, true><<<blocks, threads, 0, st>>>(c->d_tab, c->d_piola, c->nt, in, out);
-  CUDA_TRY(cudaGetLastError());
-  return HDGC_OK;
-}
-
-template <int K>
-static int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st) {
-  const int threads = 128, blocks = (c->nt + threads - 1) / threads;
-  CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
-  maxspeed2d_kernel<K><<<blocks, threads, 0, st>>>(c->d_tab, c->d_piola, c->nt, u,
-                                                   reinterpret_cast<unsigned long long*>(out));
-  CUDA_TRY(cudaGetLastError());
-  return HDGC_OK;
-}
+namespace hdgc {
+HDGC_DECLARE_ORDER(1)
+HDGC_DECLARE_ORDER(2)
+HDGC_DECLARE_ORDER(3)
+HDGC_DECLARE_ORDER(4)
+HDGC_DECLARE_ORDER(5)
+HDGC_DECLARE_ORDER(6)
+HDGC_DECLARE_ORDER(7)
+HDGC_DECLARE_ORDER(8)
+}  // namespace hdgc
 
 #define HDGC_K_SWITCH(k, CALL)                        \
   switch (k) {                                        \
@@ -290,7 +133,7 @@ static int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream
     case 6: { constexpr int KK = 6; return CALL; }    \
     case 7: { constexpr int KK = 7; return CALL; }    \
     case 8: { constexpr int KK = 8; return CALL; }    \
-    default: return set_err(HDGC_EUNSUP, "order k=%d not supported (1..8)", k); \
+    default: return hdgc_set_err(HDGC_EUNSUP, "order k=%d not supported (1..8)", k); \
   }
 
 static int elem(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
@@ -302,6 +145,30 @@ static int transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStr
   HDGC_K_SWITCH(c->k, launch_transfer<KK>(c, dir, in, out, st));
 }
 
+static int prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
+  HDGC_K_SWITCH(c->k, sf_prep<KK>(c, u, st));
+}
+
+static int sfmain(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, double dt,
+                  cudaStream_t st) {
+  HDGC_K_SWITCH(c->k, sf_main<KK>(c, mode, w, inflow, out, dt, st));
+}
+
+static int setup_variant(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& packed) {
+  HDGC_K_SWITCH(c->k, sf_setup<KK>(c, t, packed));
+}
+
+// one operator application, dispatched on the variant chosen at create
+static int apply_any(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
+                     double dt, bool prep_done, cudaStream_t st) {
+  if (c->variant == 1) {
+    int rc = prep_done ? HDGC_OK : prep(c, u, st);
+    if (rc) return rc;
+    return sfmain(c, mode, w, inflow, out, dt, st);
+  }
+  return elem(c, mode, u, w, inflow, out, dt, st);
+}
+
 // ---------------------------------------------------------------------------
 // C ABI
 
@@ -311,20 +178,20 @@ const char* hdgc_last_error(void) { return g_err.c_str(); }
 const char* hdgc_version(void) { return "hdgconv 0.1 sm_100a fp64"; }
 
 int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ctx** out) {
-  if (!mesh || !tab || !out) return set_err(HDGC_EINVAL, "null argument");
+  if (!mesh || !tab || !out) return hdgc_set_err(HDGC_EINVAL, "null argument");
   *out = nullptr;
-  if (mesh->dim != 2) return set_err(HDGC_EUNSUP, "dim=%d not supported by this build", mesh->dim);
+  if (mesh->dim != 2) return hdgc_set_err(HDGC_EUNSUP, "dim=%d not supported by this build", mesh->dim);
   const int k = tab->k;
-  if (k < 1 || k > 8) return set_err(HDGC_EUNSUP, "order k=%d not supported (1..8)", k);
+  if (k < 1 || k > 8) return hdgc_set_err(HDGC_EUNSUP, "order k=%d not supported (1..8)", k);
   if (tab->nqv != dims_nqv(k) || tab->nf != dims_nf(k))
-    return set_err(HDGC_EINVAL, "table sizes nqv=%d nf=%d do not match the k=%d rules (%d, %d)",
+    return hdgc_set_err(HDGC_EINVAL, "table sizes nqv=%d nf=%d do not match the k=%d rules (%d, %d)",
                    tab->nqv, tab->nf, k, dims_nqv(k), dims_nf(k));
   if (mesh->n_elements <= 0 || mesh->n_vertices <= 0 || mesh->n_facets <= 0)
-    return set_err(HDGC_EINVAL, "empty mesh");
-  if ((int64_t)mesh->n_elements * 4 > INT32_MAX) return set_err(HDGC_EINVAL, "too many elements");
+    return hdgc_set_err(HDGC_EINVAL, "empty mesh");
+  if ((int64_t)mesh->n_elements * 4 > INT32_MAX) return hdgc_set_err(HDGC_EINVAL, "too many elements");
   if (!mesh->vertices || !mesh->elements || !mesh->facet_elems || !mesh->facet_local || !tab->coef || !tab->div_modal ||
       !tab->vol_w || !tab->vol_D || !tab->vol_G || !tab->fac_w || !tab->fac_L || !tab->fac_D || !tab->fac_len)
-    return set_err(HDGC_EINVAL, "null array in descriptor");
+    return hdgc_set_err(HDGC_EINVAL, "null array in descriptor");
 
   hdgc_ctx* c = new hdgc_ctx();
   c->dim = 2;
@@ -362,13 +229,14 @@ int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ct
     hdgc_destroy(c);
     return code;
   };
-  if ((rc = dev_alloc(c, (void**)&c->d_tab, h.size() * sizeof(double)))) return fail(rc);
-  if ((rc = dev_alloc(c, (void**)&c->d_code, NT * 3 * sizeof(int32_t)))) return fail(rc);
-  if ((rc = dev_alloc(c, (void**)&c->d_piola, NT * 4 * sizeof(double)))) return fail(rc);
-  if ((rc = dev_alloc(c, (void**)&c->d_minv, NT * sizeof(double)))) return fail(rc);
-  if ((rc = dev_alloc(c, (void**)&c->d_scratch, NT * nb * sizeof(double)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_tab, h.size() * sizeof(double)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_code, NT * 3 * sizeof(int32_t)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_piola, NT * 4 * sizeof(double)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_minv, NT * sizeof(double)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_scratch, NT * nb * sizeof(double)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_modal, NT * (nb + k * (k + 1) / 2) * sizeof(double)))) return fail(rc);
 #define SETUP_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) \
-    return fail(set_err(HDGC_ECUDA, "%s: %s", #x, cudaGetErrorString(e_))); } while (0)
+    return fail(hdgc_set_err(HDGC_ECUDA, "%s: %s", #x, cudaGetErrorString(e_))); } while (0)
   SETUP_TRY(cudaMemcpy(c->d_tab, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
   SETUP_TRY(cudaMalloc(&d_V, sizeof(double) * 2 * c->nv));
   SETUP_TRY(cudaMalloc(&d_tri, sizeof(int64_t) * 3 * NT));
@@ -392,9 +260,10 @@ int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ct
   }
   int misc[2];
   SETUP_TRY(cudaMemcpy(misc, d_misc, sizeof(misc), cudaMemcpyDeviceToHost));
-  if (misc[1] == 1) return fail(set_err(HDGC_EINVAL, "inverted or degenerate element (detJ <= 0)"));
-  if (misc[1] == 2) return fail(set_err(HDGC_EINVAL, "invalid facet_elems/facet_local entry"));
+  if (misc[1] == 1) return fail(hdgc_set_err(HDGC_EINVAL, "inverted or degenerate element (detJ <= 0)"));
+  if (misc[1] == 2) return fail(hdgc_set_err(HDGC_EINVAL, "invalid facet_elems/facet_local entry"));
   c->nbf = misc[0];
+  if ((rc = setup_variant(c, tab, h))) return fail(rc);
   cudaFree(d_V); cudaFree(d_tri); cudaFree(d_fe); cudaFree(d_fl); cudaFree(d_slot);
   *out = c;
   return HDGC_OK;
@@ -404,13 +273,13 @@ int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ct
 int hdgc_destroy(hdgc_ctx* c) {
   if (!c) return HDGC_OK;
   cudaFree(c->d_tab); cudaFree(c->d_code); cudaFree(c->d_piola); cudaFree(c->d_minv);
-  cudaFree(c->d_scratch); cudaFree(c->d_hu); cudaFree(c->d_hw); cudaFree(c->d_hr); cudaFree(c->d_hin);
+  cudaFree(c->d_scratch); cudaFree(c->d_scratch2); cudaFree(c->d_modal); cudaFree(c->d_prep); cudaFree(c->d_ftab); cudaFree(c->d_hu); cudaFree(c->d_hw); cudaFree(c->d_hr); cudaFree(c->d_hin);
   delete c;
   return HDGC_OK;
 }
 
 int hdgc_get_info(const hdgc_ctx* c, hdgc_info* info) {
-  if (!c || !info) return set_err(HDGC_EINVAL, "null argument");
+  if (!c || !info) return hdgc_set_err(HDGC_EINVAL, "null argument");
   info->dim = c->dim; info->k = c->k; info->nb = c->nb; info->nbs = c->nbs;
   info->nqv = c->nqv; info->nf = c->nf;
   info->n_elements = c->nt; info->n_facets = c->nf_facets; info->n_boundary_facets = c->nbf;
@@ -420,30 +289,40 @@ int hdgc_get_info(const hdgc_ctx* c, hdgc_info* info) {
 }
 
 int hdgc_apply_v(hdgc_ctx* c, const double* u, const double* w, const double* inflow, double* r, void* stream) {
-  if (!c || !u || !w || !r) return set_err(HDGC_EINVAL, "null argument");
-  if (r == u || r == w || r == inflow) return set_err(HDGC_EINVAL, "output aliases an input");
-  return elem(c, MODE_APPLY, u, w, inflow, r, 0.0, (cudaStream_t)stream);
+  if (!c || !u || !w || !r) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (r == u || r == w || r == inflow) return hdgc_set_err(HDGC_EINVAL, "output aliases an input");
+  return apply_any(c, MODE_APPLY, u, w, inflow, r, 0.0, false, (cudaStream_t)stream);
 }
 
 int hdgc_apply_w(hdgc_ctx* c, const double* u, const double* inflow, double* r_w, void* stream) {
-  if (!c || !u || !r_w) return set_err(HDGC_EINVAL, "null argument");
-  if (r_w == u || r_w == inflow) return set_err(HDGC_EINVAL, "output aliases an input");
+  if (!c || !u || !r_w) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (r_w == u || r_w == inflow) return hdgc_set_err(HDGC_EINVAL, "output aliases an input");
   cudaStream_t st = (cudaStream_t)stream;
   int rc = transfer(c, 0, u, c->d_scratch, st);
   if (rc) return rc;
-  return elem(c, MODE_APPLY_IT, u, c->d_scratch, inflow, r_w, 0.0, st);
+  if (c->variant == 0) return elem(c, MODE_APPLY_IT, u, c->d_scratch, inflow, r_w, 0.0, st);
+  // sum-factorised: r_V into scratch2, then I^T
+  if (!c->d_scratch2 &&
+      (rc = hdgc_dev_alloc(c, (void**)&c->d_scratch2, sizeof(double) * (size_t)c->nt * c->nb)))
+    return rc;
+  if ((rc = apply_any(c, MODE_APPLY, u, c->d_scratch, inflow, c->d_scratch2, 0.0, false, st))) return rc;
+  return transfer(c, 1, c->d_scratch2, r_w, st);
 }
 
 int hdgc_substeps(hdgc_ctx* c, const double* u, double* w, const double* inflow, double dt, int32_t nsteps,
                   void* stream) {
-  if (!c || !u || !w) return set_err(HDGC_EINVAL, "null argument");
-  if (nsteps < 0) return set_err(HDGC_EINVAL, "nsteps < 0");
-  if (w == u || w == inflow) return set_err(HDGC_EINVAL, "w aliases an input");
+  if (!c || !u || !w) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (nsteps < 0) return hdgc_set_err(HDGC_EINVAL, "nsteps < 0");
+  if (w == u || w == inflow) return hdgc_set_err(HDGC_EINVAL, "w aliases an input");
   cudaStream_t st = (cudaStream_t)stream;
   double* a = w;
   double* b = c->d_scratch;
+  if (nsteps > 0 && c->variant == 1) {
+    int rc = prep(c, u, st);    // u is frozen over the substep batch
+    if (rc) return rc;
+  }
   for (int s = 0; s < nsteps; ++s) {
-    int rc = elem(c, MODE_SUBSTEP, u, a, inflow, b, dt, st);
+    int rc = apply_any(c, MODE_SUBSTEP, u, a, inflow, b, dt, true, st);
     if (rc) return rc;
     double* t = a; a = b; b = t;
   }
@@ -452,37 +331,37 @@ int hdgc_substeps(hdgc_ctx* c, const double* u, double* w, const double* inflow,
 }
 
 int hdgc_transfer(hdgc_ctx* c, int32_t direction, const double* in, double* out, void* stream) {
-  if (!c || !in || !out) return set_err(HDGC_EINVAL, "null argument");
-  if (in == out) return set_err(HDGC_EINVAL, "output aliases input");
-  if (direction != 0 && direction != 1) return set_err(HDGC_EINVAL, "direction must be 0 (I) or 1 (I^T)");
+  if (!c || !in || !out) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (in == out) return hdgc_set_err(HDGC_EINVAL, "output aliases input");
+  if (direction != 0 && direction != 1) return hdgc_set_err(HDGC_EINVAL, "direction must be 0 (I) or 1 (I^T)");
   return transfer(c, direction, in, out, (cudaStream_t)stream);
 }
 
 int hdgc_mass_inverse(hdgc_ctx* c, double* out, void* stream) {
-  if (!c || !out) return set_err(HDGC_EINVAL, "null argument");
+  if (!c || !out) return hdgc_set_err(HDGC_EINVAL, "null argument");
   CUDA_TRY(cudaMemcpyAsync(out, c->d_minv, sizeof(double) * c->nt, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   return HDGC_OK;
 }
 
 int hdgc_max_speed(hdgc_ctx* c, const double* u, double* out_dev, void* stream) {
-  if (!c || !u || !out_dev) return set_err(HDGC_EINVAL, "null argument");
+  if (!c || !u || !out_dev) return hdgc_set_err(HDGC_EINVAL, "null argument");
   HDGC_K_SWITCH(c->k, launch_maxspeed<KK>(c, u, out_dev, (cudaStream_t)stream));
 }
 
 static int ensure_staging(hdgc_ctx* c, bool need_inflow) {
   const size_t vec = sizeof(double) * (size_t)c->nt * c->nb;
   int rc;
-  if (!c->d_hu && (rc = dev_alloc(c, (void**)&c->d_hu, vec))) return rc;
-  if (!c->d_hw && (rc = dev_alloc(c, (void**)&c->d_hw, vec))) return rc;
-  if (!c->d_hr && (rc = dev_alloc(c, (void**)&c->d_hr, vec))) return rc;
+  if (!c->d_hu && (rc = hdgc_dev_alloc(c, (void**)&c->d_hu, vec))) return rc;
+  if (!c->d_hw && (rc = hdgc_dev_alloc(c, (void**)&c->d_hw, vec))) return rc;
+  if (!c->d_hr && (rc = hdgc_dev_alloc(c, (void**)&c->d_hr, vec))) return rc;
   if (need_inflow && !c->d_hin && c->nbf > 0 &&
-      (rc = dev_alloc(c, (void**)&c->d_hin, sizeof(double) * (size_t)c->nbf * c->nf * 2)))
+      (rc = hdgc_dev_alloc(c, (void**)&c->d_hin, sizeof(double) * (size_t)c->nbf * c->nf * 2)))
     return rc;
   return HDGC_OK;
 }
 
 int hdgc_apply_v_host(hdgc_ctx* c, const double* u, const double* w, const double* inflow, double* r, void* stream) {
-  if (!c || !u || !w || !r) return set_err(HDGC_EINVAL, "null argument");
+  if (!c || !u || !w || !r) return hdgc_set_err(HDGC_EINVAL, "null argument");
   int rc = ensure_staging(c, inflow != nullptr);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -494,7 +373,7 @@ int hdgc_apply_v_host(hdgc_ctx* c, const double* u, const double* w, const doubl
     CUDA_TRY(cudaMemcpyAsync(c->d_hin, inflow, sizeof(double) * (size_t)c->nbf * c->nf * 2, cudaMemcpyHostToDevice, st));
     din = c->d_hin;
   }
-  if ((rc = elem(c, MODE_APPLY, c->d_hu, c->d_hw, din, c->d_hr, 0.0, st))) return rc;
+  if ((rc = apply_any(c, MODE_APPLY, c->d_hu, c->d_hw, din, c->d_hr, 0.0, false, st))) return rc;
   CUDA_TRY(cudaMemcpyAsync(r, c->d_hr, vec, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return HDGC_OK;
@@ -502,7 +381,7 @@ int hdgc_apply_v_host(hdgc_ctx* c, const double* u, const double* w, const doubl
 
 int hdgc_substeps_host(hdgc_ctx* c, const double* u, double* w, const double* inflow, double dt, int32_t nsteps,
                        void* stream) {
-  if (!c || !u || !w) return set_err(HDGC_EINVAL, "null argument");
+  if (!c || !u || !w) return hdgc_set_err(HDGC_EINVAL, "null argument");
   int rc = ensure_staging(c, inflow != nullptr);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;

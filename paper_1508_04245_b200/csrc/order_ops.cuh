@@ -1,0 +1,284 @@
+// order_ops.cuh — per-order kernel launchers (included by order_k<K>.cu only).
+#pragma once
+#include <cstring>
+
+#include "context.cuh"
+#include "conv2d_thread.cuh"
+#include "conv2d_sf.cuh"
+
+namespace hdgc {
+
+// ---------------------------------------------------------------------------
+// small per-element matrix-vector products, one thread per (element, row):
+// no large unrolled blocks, so every order compiles in seconds.
+
+// modal velocity data: out[T][r] = sum_j M[r][j] u[T][j], M = [coef ; divm]
+// (u_hat = coef u, PB:357-378; div u_hat in the P_{k-1} Dubiner modes)
+template <int K>
+__global__ void __launch_bounds__(256)
+rowmat2d_kernel(const double* __restrict__ tab, const double* __restrict__ u, int nt,
+                double* __restrict__ out) {
+  using D = Dims<K>;
+  constexpr int NB = D::NB, R = D::NB + D::NBS1;
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)nt * R) return;
+  const int T = (int)(gid / R);
+  const int r = (int)(gid - (long long)T * R);
+  const double* M = tab + D::OFF_COEF + (size_t)r * NB;   // coef rows then divm rows (contiguous)
+  const double* x = u + (size_t)T * NB;
+  double a = 0.0;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) a = fma(__ldg(M + j), __ldg(x + j), a);
+  out[gid] = a;
+}
+
+// I (BDM -> V_h): w[c*nbs+m] = sum_d P[c][d] (coef u)[d*nbs+m]
+// I^T:            r_w[j]     = sum_{d,m} coef[d*nbs+m][j] sum_c P[c][d] r[c*nbs+m]
+// one thread per (element, output row); in and out must not alias.
+template <int K, bool TRANSPOSE>
+__global__ void __launch_bounds__(256)
+transfer2d_kernel(const double* __restrict__ tab, const double* __restrict__ piola, int nt,
+                  const double* __restrict__ in, double* __restrict__ out) {
+  using D = Dims<K>;
+  constexpr int NB = D::NB, NBS = D::NBS;
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)nt * NB) return;
+  const int T = (int)(gid / NB);
+  const int r = (int)(gid - (long long)T * NB);
+  const double P00 = __ldg(piola + T), P01 = __ldg(piola + (size_t)nt + T);
+  const double P10 = __ldg(piola + 2 * (size_t)nt + T), P11 = __ldg(piola + 3 * (size_t)nt + T);
+  const double* coef = tab + D::OFF_COEF;
+  const double* x = in + (size_t)T * NB;
+  if (!TRANSPOSE) {
+    const int c = r >= NBS ? 1 : 0, m = r - c * NBS;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const double xj = __ldg(x + j);
+      a0 = fma(__ldg(coef + (size_t)m * NB + j), xj, a0);
+      a1 = fma(__ldg(coef + (size_t)(NBS + m) * NB + j), xj, a1);
+    }
+    out[gid] = c == 0 ? fma(P00, a0, P01 * a1) : fma(P10, a0, P11 * a1);
+  } else {
+    double a = 0.0;
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) {
+      const double x0 = __ldg(x + m), x1 = __ldg(x + NBS + m);
+      a = fma(__ldg(coef + (size_t)m * NB + r), fma(P00, x0, P10 * x1), a);
+      a = fma(__ldg(coef + (size_t)(NBS + m) * NB + r), fma(P01, x0, P11 * x1), a);
+    }
+    out[gid] = a;
+  }
+}
+
+// max |J u_hat / detJ| over elements x volume points, one thread per
+// (element, point), from the modal rows; positive doubles order as uint64
+template <int K>
+__global__ void __launch_bounds__(256)
+maxspeed2d_kernel(const double* __restrict__ tab, const double* __restrict__ piola, int nt,
+                  const double* __restrict__ modal, unsigned long long* __restrict__ out) {
+  using D = Dims<K>;
+  constexpr int NBS = D::NBS, MR = D::NB + D::NBS1, NQV = D::NQV;
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double best = 0.0;
+  if (gid < (long long)nt * NQV) {
+    const int T = (int)(gid / NQV);
+    const int q = (int)(gid - (long long)T * NQV);
+    const double* mr = modal + (size_t)T * MR;
+    const double* Dq = tab + D::OFF_VD + q * NBS;
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) {
+      const double d = __ldg(Dq + m);
+      a = fma(__ldg(mr + m), d, a);
+      b = fma(__ldg(mr + NBS + m), d, b);
+    }
+    const double P00 = __ldg(piola + T), P01 = __ldg(piola + (size_t)nt + T);
+    const double P10 = __ldg(piola + 2 * (size_t)nt + T), P11 = __ldg(piola + 3 * (size_t)nt + T);
+    const double x = fma(P00, a, P01 * b), y = fma(P10, a, P11 * b);
+    best = sqrt(fma(x, x, y * y));
+  }
+  for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
+}
+
+static inline unsigned grid_for(long long work, int threads) { return (unsigned)((work + threads - 1) / threads); }
+
+template <int K>
+int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow,
+                       double* out, double dt, cudaStream_t st) {
+ if constexpr (K > 2) {
+  (void)c; (void)mode; (void)u; (void)w; (void)inflow; (void)out; (void)dt; (void)st;
+  return hdgc_set_err(HDGC_EUNSUP, "thread-per-element variant is built for k <= 2 only");
+ } else {
+  ElemParams p;
+  p.tab = c->d_tab;
+  p.u = u;
+  p.w = w;
+  p.inflow = inflow;
+  p.code = c->d_code;
+  p.piola = c->d_piola;
+  p.minv = c->d_minv;
+  p.out = out;
+  p.dt = dt;
+  p.nt = c->nt;
+  const int threads = 128;
+  const int blocks = (c->nt + threads - 1) / threads;
+  const int smem = thread_smem_bytes<K>();
+  auto launch = [&](auto kern) -> int {
+    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<blocks, threads, smem, st>>>(p);
+    CUDA_TRY(cudaGetLastError());
+    return HDGC_OK;
+  };
+  switch (mode) {
+    case MODE_APPLY: return launch(conv2d_thread_kernel<K, MODE_APPLY>);
+    case MODE_SUBSTEP: return launch(conv2d_thread_kernel<K, MODE_SUBSTEP>);
+    default: return launch(conv2d_thread_kernel<K, MODE_APPLY_IT>);
+  }
+ }
+}
+
+template <int K>
+int launch_transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st) {
+  const long long work = (long long)c->nt * Dims<K>::NB;
+  if (dir == 0) transfer2d_kernel<K, false><<<grid_for(work, 256), 256, 0, st>>>(c->d_tab, c->d_piola, c->nt, in, out);
+  else transfer2d_kernel<K, true><<<grid_for(work, 256), 256, 0, st>>>(c->d_tab, c->d_piola, c->nt, in, out);
+  CUDA_TRY(cudaGetLastError());
+  return HDGC_OK;
+}
+
+// modal rows u_hat | div u_hat into c->d_modal
+template <int K>
+int launch_modal(hdgc_ctx* c, const double* u, cudaStream_t st) {
+  const long long work = (long long)c->nt * (Dims<K>::NB + Dims<K>::NBS1);
+  rowmat2d_kernel<K><<<grid_for(work, 256), 256, 0, st>>>(c->d_tab, u, c->nt, c->d_modal);
+  CUDA_TRY(cudaGetLastError());
+  return HDGC_OK;
+}
+
+template <int K>
+int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st) {
+  int rc = launch_modal<K>(c, u, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
+  const long long work = (long long)c->nt * Dims<K>::NQV;
+  maxspeed2d_kernel<K><<<grid_for(work, 256), 256, 0, st>>>(c->d_tab, c->d_piola, c->nt, c->d_modal,
+                                                           reinterpret_cast<unsigned long long*>(out));
+  CUDA_TRY(cudaGetLastError());
+  return HDGC_OK;
+}
+
+// frozen-velocity prep rows (alpha | beta | gamma | s) into c->d_prep
+template <int K>
+int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
+  if constexpr (K >= 3 && K <= 6) {
+    prep_fused2d_kernel<K><<<grid_for(c->nt, 128), 128, 0, st>>>(u, c->nt, c->d_prep);
+    CUDA_TRY(cudaGetLastError());
+    return HDGC_OK;
+  } else if constexpr (K >= 3) {
+    int rc = launch_modal<K>(c, u, st);
+    if (rc) return rc;
+    const long long work = (long long)c->nt * SF<K>::PREP;
+    prep_points2d_kernel<K><<<grid_for(work, 256), 256, 0, st>>>(c->d_tab, u, c->d_modal, c->nt, c->d_prep);
+    CUDA_TRY(cudaGetLastError());
+    return HDGC_OK;
+  } else {
+    (void)c; (void)u; (void)st;
+    return hdgc_set_err(HDGC_EUNSUP, "sum-factorised variant needs k >= 3");
+  }
+}
+
+template <int K>
+int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, double dt,
+                   cudaStream_t st) {
+  if constexpr (K >= 3) {
+    using F = SF<K>;
+    SFParams p;
+    p.prep = c->d_prep;
+    p.w = w;
+    p.inflow = inflow;
+    p.code = c->d_code;
+    p.minv = c->d_minv;
+    p.ftab = c->d_ftab;
+    p.out = out;
+    p.dt = dt;
+    p.nt = c->nt;
+    const int smem = F::SMEM_DOUBLES * (int)sizeof(double);
+    const int blocks = (c->nt + F::EPB - 1) / F::EPB;
+    auto launch = [&](auto kern) -> int {
+      if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<blocks, F::THREADS, smem, st>>>(p);
+      CUDA_TRY(cudaGetLastError());
+      return HDGC_OK;
+    };
+    if (mode == MODE_SUBSTEP) return launch(conv2d_sf_kernel<K, MODE_SUBSTEP>);
+    return launch(conv2d_sf_kernel<K, MODE_APPLY>);
+  } else {
+    return hdgc_set_err(HDGC_EUNSUP, "sum-factorised variant needs k >= 3");
+  }
+}
+
+// upload the sum-factorisation tables (constant bank) and facet tables
+template <int K>
+int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& packed) {
+  if constexpr (K >= 3) {
+    using F = SF<K>;
+    using D = Dims<K>;
+    if (t->col_n != F::N || !t->col_A || !t->col_Ad || !t->col_B || !t->col_Bd || !t->col_xi ||
+        !t->col_wa || !t->col_wy || !t->col_inv1my)
+      return hdgc_set_err(HDGC_EINVAL, "collapsed (sum-factorisation) tables missing or n=%d != %d", t->col_n, F::N);
+    std::vector<double> h(F::C_TOTAL);
+    memcpy(&h[F::C_A], t->col_A, sizeof(double) * F::N * F::NE);
+    memcpy(&h[F::C_AD], t->col_Ad, sizeof(double) * F::N * F::NE);
+    memcpy(&h[F::C_B], t->col_B, sizeof(double) * F::N * F::NBS);
+    memcpy(&h[F::C_BD], t->col_Bd, sizeof(double) * F::N * F::NBS);
+    // per-point factors of alpha/beta/gamma: point p = b*n + a (collapsed rule order)
+    for (int b = 0; b < F::N; ++b)
+      for (int a = 0; a < F::N; ++a) {
+        const double wp = t->col_wa[a] * t->col_wy[b];
+        h[F::C_PA + b * F::N + a] = wp * t->col_inv1my[b];
+        h[F::C_PB + b * F::N + a] = wp * t->col_xi[a] * t->col_inv1my[b];
+        h[F::C_PW + b * F::N + a] = wp;
+      }
+    CUDA_TRY(cudaMemcpyToSymbol(c_sf, h.data(), sizeof(double) * F::C_TOTAL));
+    std::vector<double> ft(F::TAB_PAD, 0.0);
+    memcpy(&ft[0], &packed[D::OFF_FD], sizeof(double) * 3 * F::NF * F::NBS);
+    CUDA_TRY(cudaMemcpyToSymbol(c_fd, ft.data(), sizeof(double) * F::TAB));
+#if HDGC_CM_FUSED
+    {
+      // [coef ; divm] | fL | fw | flen for the fused prep kernel
+      std::vector<double> cm((F::NB + F::NBS1) * F::NB + F::NF * F::NE + F::NF + 3);
+      memcpy(&cm[0], &packed[D::OFF_COEF], sizeof(double) * (F::NB + F::NBS1) * F::NB);
+      size_t o2 = (size_t)(F::NB + F::NBS1) * F::NB;
+      memcpy(&cm[o2], &packed[D::OFF_FL], sizeof(double) * F::NF * F::NE); o2 += F::NF * F::NE;
+      memcpy(&cm[o2], &packed[D::OFF_FW], sizeof(double) * F::NF); o2 += F::NF;
+      memcpy(&cm[o2], &packed[D::OFF_FLEN], sizeof(double) * 3);
+      CUDA_TRY(cudaMemcpyToSymbol(c_cm, cm.data(), sizeof(double) * cm.size()));
+    }
+#endif
+    int rc = hdgc_dev_alloc(c, (void**)&c->d_ftab, sizeof(double) * F::TAB_PAD);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpy(c->d_ftab, ft.data(), sizeof(double) * F::TAB_PAD, cudaMemcpyHostToDevice));
+    rc = hdgc_dev_alloc(c, (void**)&c->d_prep, sizeof(double) * (size_t)c->nt * F::PREP_PAD);
+    if (rc) return rc;
+    c->variant = 1;
+    return HDGC_OK;
+  } else {
+    (void)c; (void)t; (void)packed;
+    return HDGC_OK;
+  }
+}
+
+}  // namespace hdgc
+
+#define HDGC_INSTANTIATE_ORDER(K)                                                                 \
+  namespace hdgc {                                                                                \
+  template int launch_elem<K>(hdgc_ctx*, int, const double*, const double*, const double*, double*, \
+                              double, cudaStream_t);                                              \
+  template int launch_transfer<K>(hdgc_ctx*, int, const double*, double*, cudaStream_t);          \
+  template int launch_maxspeed<K>(hdgc_ctx*, const double*, double*, cudaStream_t);               \
+  template int sf_prep<K>(hdgc_ctx*, const double*, cudaStream_t);                                \
+  template int sf_main<K>(hdgc_ctx*, int, const double*, const double*, double*, double, cudaStream_t); \
+  template int sf_setup<K>(hdgc_ctx*, const hdgc_tables_desc*, const std::vector<double>&);        \
+  }

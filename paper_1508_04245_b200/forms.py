@@ -139,9 +139,15 @@ class ConvectionOperator:
             facet_elems=arr(mesh.facet_elems, np.int64), facet_local=arr(mesh.facet_local, np.int64),
             facet_perm=None)
         td = _lib.TablesDesc(
-            k=self.k, nqv=self.nqv, nf=self.nf, coef=arr(tab["coef"]), div_modal=arr(tab["div_modal"]), vol_w=arr(tab["vol_w"]),
-            vol_D=arr(tab["vol_D"]), vol_G=arr(tab["vol_G"]), fac_w=arr(tab["fac_w"]),
-            fac_L=arr(tab["fac_L"]), fac_D=arr(tab["fac_D"]), fac_len=arr(tab["fac_len"]))
+            k=self.k, nqv=self.nqv, nf=self.nf, coef=arr(tab["coef"]), div_modal=arr(tab["div_modal"]),
+            vol_w=arr(tab["vol_w"]), vol_D=arr(tab["vol_D"]), vol_G=arr(tab["vol_G"]),
+            fac_w=arr(tab["fac_w"]), fac_L=arr(tab["fac_L"]), fac_D=arr(tab["fac_D"]),
+            fac_len=arr(tab["fac_len"]))
+        if self.k >= 3:
+            ct = B.collapsed_tables(self.k)
+            td.col_n = ct["n"]
+            for name in ("A", "Ad", "B", "Bd", "xi", "wa", "wy", "inv1my"):
+                setattr(td, "col_" + name, arr(ct[name]))
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("ConvectionOperator needs a CUDA device (no CPU fallback)")
