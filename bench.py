@@ -243,16 +243,10 @@ def main():
     dofs_per_step = NT * nb * NSUB
     value = world * dofs_per_step / t_step
 
-    # ---- per-launch duration of the substep kernel (L2 state as inside a step)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(50)]
-    wd.copy_(w0)
-    op.substeps(ud, wd, dt, 2, infd)
-    for a, b in kev:
-        a.record(stream)
-        op.substeps(ud, wd, dt, 1, infd)
-        b.record(stream)
-    torch.cuda.synchronize()
-    k_s = statistics.median(a.elapsed_time(b) * 1e-3 for a, b in kev)
+    # ---- average launch duration of the dominant (substep) kernel: the step is
+    # one frozen-velocity prep launch + NSUB substep launches back to back on
+    # this stream, so step time / NSUB bounds it from above (prep amortised in)
+    k_s = t_step / NSUB
 
     # ---- e2e through the public API with pinned HOST buffers (H2D + 100 substeps + D2H)
     uh = torch.from_numpy(u).pin_memory().numpy()
@@ -303,7 +297,7 @@ def main():
         "e2e": {"value": world * dofs_per_step / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": int(u.nbytes + w.nbytes + inflow.nbytes),
                 "d2h_bytes_per_step": int(w.nbytes)},
-        "gpu_launches": args.steps * NSUB,
+        "gpu_launches": args.steps * (NSUB + 1),   # per step: 1 prep + NSUB substep kernels
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
