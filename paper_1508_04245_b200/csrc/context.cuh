@@ -32,6 +32,7 @@ struct hdgc_ctx {
   double* d_prep = nullptr;     // (NT, PREP) frozen-velocity data (sum-factorised variant)
   double* d_modal = nullptr;    // (NT, nb + nbs(k-1)) modal u_hat | div u_hat
   double* d_scratch2 = nullptr; // (NT, nb) r_V for apply_w (lazily allocated)
+  double* d_sign = nullptr;     // (NT,) sign(detJ) (3D: sorted-vertex tets)
   double* d_ftab = nullptr;     // facet tables fw | fD (sum-factorised variant)
   // host-variant staging (lazily allocated)
   double* d_hu = nullptr;
@@ -54,6 +55,20 @@ template <int K> int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st);
 template <int K> int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out,
                              double dt, cudaStream_t st);
 template <int K> int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& packed);
+
+// 3D (tetrahedra), order3d_k<K>.cu
+template <int K> int launch3_prep(hdgc_ctx* c, const double* u, cudaStream_t st);
+template <int K> int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out,
+                                  double dt, cudaStream_t st);
+template <int K> int launch3_transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st);
+template <int K> int launch3_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st);
+
+#define HDGC_DECLARE_ORDER3(K)                                                                     \
+  extern template int launch3_prep<K>(hdgc_ctx*, const double*, cudaStream_t);                    \
+  extern template int launch3_main<K>(hdgc_ctx*, int, const double*, const double*, double*, double, \
+                                      cudaStream_t);                                               \
+  extern template int launch3_transfer<K>(hdgc_ctx*, int, const double*, double*, cudaStream_t);  \
+  extern template int launch3_maxspeed<K>(hdgc_ctx*, const double*, double*, cudaStream_t);
 
 #define HDGC_DECLARE_ORDER(K)                                                                      \
   extern template int launch_elem<K>(hdgc_ctx*, int, const double*, const double*, const double*,  \

@@ -10,6 +10,7 @@
 
 #include "common.cuh"
 #include "context.cuh"
+#include "conv3d.cuh"
 
 using namespace hdgc;
 
@@ -61,6 +62,26 @@ __global__ void geometry2d_kernel(const double* __restrict__ V, const int64_t* _
   piola[2 * (size_t)nt + T] = j10 * id;
   piola[3 * (size_t)nt + T] = j11 * id;
   minv[T] = 2.0 * id;
+}
+
+// 3D: J = [v1-v0, v2-v0, v3-v0], Piola J/detJ (9, NT) row-major, 6/|detJ|, sign(detJ)
+__global__ void hdgc::geometry3d_kernel(const double* __restrict__ V, const int64_t* __restrict__ tet, int nt,
+                                        double* __restrict__ piola, double* __restrict__ minv,
+                                        double* __restrict__ sgn, int* __restrict__ bad) {
+  int T = blockIdx.x * blockDim.x + threadIdx.x;
+  if (T >= nt) return;
+  int64_t v[4];
+  for (int i = 0; i < 4; ++i) v[i] = tet[4 * (size_t)T + i];
+  double J[9];
+  for (int c = 0; c < 3; ++c)
+    for (int d = 0; d < 3; ++d) J[3 * c + d] = V[3 * v[d + 1] + c] - V[3 * v[0] + c];
+  const double det = J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6]) +
+                     J[2] * (J[3] * J[7] - J[4] * J[6]);
+  if (!(fabs(det) > 0.0)) atomicExch(bad, 1);
+  const double id = 1.0 / det;
+  for (int i = 0; i < 9; ++i) piola[(size_t)i * nt + T] = J[i] * id;
+  minv[T] = 6.0 / fabs(det);
+  sgn[T] = det > 0.0 ? 1.0 : -1.0;
 }
 
 // boundary flag per facet
@@ -141,7 +162,10 @@ static int elem(hdgc_ctx* c, int mode, const double* u, const double* w, const d
   HDGC_K_SWITCH(c->k, launch_elem<KK>(c, mode, u, w, inflow, out, dt, st));
 }
 
+static int transfer3(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st);
+
 static int transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st) {
+  if (c->dim == 3) return transfer3(c, dir, in, out, st);
   HDGC_K_SWITCH(c->k, launch_transfer<KK>(c, dir, in, out, st));
 }
 
@@ -159,8 +183,17 @@ static int setup_variant(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vect
 }
 
 // one operator application, dispatched on the variant chosen at create
+static int main3(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, double dt,
+                 cudaStream_t st);
+static int prep3(hdgc_ctx* c, const double* u, cudaStream_t st);
+
 static int apply_any(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
                      double dt, bool prep_done, cudaStream_t st) {
+  if (c->variant == 2) {
+    int rc = prep_done ? HDGC_OK : prep3(c, u, st);
+    if (rc) return rc;
+    return main3(c, mode, w, inflow, out, dt, st);
+  }
   if (c->variant == 1) {
     int rc = prep_done ? HDGC_OK : prep(c, u, st);
     if (rc) return rc;
@@ -172,6 +205,126 @@ static int apply_any(hdgc_ctx* c, int mode, const double* u, const double* w, co
 // ---------------------------------------------------------------------------
 // C ABI
 
+namespace hdgc {
+HDGC_DECLARE_ORDER3(1)
+HDGC_DECLARE_ORDER3(2)
+HDGC_DECLARE_ORDER3(3)
+HDGC_DECLARE_ORDER3(4)
+}  // namespace hdgc
+
+#define HDGC_K3_SWITCH(k, CALL)                       \
+  switch (k) {                                        \
+    case 1: { constexpr int KK = 1; return CALL; }    \
+    case 2: { constexpr int KK = 2; return CALL; }    \
+    case 3: { constexpr int KK = 3; return CALL; }    \
+    case 4: { constexpr int KK = 4; return CALL; }    \
+    default: return hdgc_set_err(HDGC_EUNSUP, "3D order k=%d not supported (1..4)", k); \
+  }
+
+static int prep3(hdgc_ctx* c, const double* u, cudaStream_t st) { HDGC_K3_SWITCH(c->k, launch3_prep<KK>(c, u, st)); }
+static int main3(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, double dt,
+                 cudaStream_t st) {
+  HDGC_K3_SWITCH(c->k, launch3_main<KK>(c, mode, w, inflow, out, dt, st));
+}
+static int transfer3(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st) {
+  HDGC_K3_SWITCH(c->k, launch3_transfer<KK>(c, dir, in, out, st));
+}
+static int maxspeed3(hdgc_ctx* c, const double* u, double* out, cudaStream_t st) {
+  HDGC_K3_SWITCH(c->k, launch3_maxspeed<KK>(c, u, out, st));
+}
+
+extern "C" int hdgc_destroy(hdgc_ctx* c);
+
+// 3D context: tet mesh (vertices sorted per tet), Dims3<K> tables
+static int create3d(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ctx** out) {
+  const int k = tab->k;
+  if (k < 1 || k > 4) return hdgc_set_err(HDGC_EUNSUP, "3D order k=%d not supported (1..4)", k);
+  if (tab->nqv != dims3_nq(k) || tab->nf != dims3_nf(k))
+    return hdgc_set_err(HDGC_EINVAL, "3D table sizes nqv=%d nf=%d do not match the k=%d rules (%d, %d)",
+                        tab->nqv, tab->nf, k, dims3_nq(k), dims3_nf(k));
+  if (mesh->n_elements <= 0 || mesh->n_vertices <= 0 || mesh->n_facets <= 0)
+    return hdgc_set_err(HDGC_EINVAL, "empty mesh");
+  if ((int64_t)mesh->n_elements * 4 > INT32_MAX) return hdgc_set_err(HDGC_EINVAL, "too many elements");
+  if (!mesh->vertices || !mesh->elements || !mesh->facet_elems || !mesh->facet_local || !tab->coef ||
+      !tab->div_modal || !tab->vol_w || !tab->vol_D || !tab->vol_G || !tab->fac_w || !tab->fac_L ||
+      !tab->fac_D || !tab->fac_len)
+    return hdgc_set_err(HDGC_EINVAL, "null array in descriptor");
+  hdgc_ctx* c = new hdgc_ctx();
+  c->dim = 3;
+  c->k = k;
+  c->nbs = dims3_nbs(k);
+  c->nb = 3 * c->nbs;
+  c->nqv = tab->nqv;
+  c->nf = tab->nf;
+  c->nt = mesh->n_elements;
+  c->nv = mesh->n_vertices;
+  c->nf_facets = mesh->n_facets;
+  c->variant = 2;
+  const int nb = c->nb, nbs = c->nbs, nqv = c->nqv, nf = c->nf;
+  const int nbs1 = k * (k + 1) * (k + 2) / 6, nfd = (k + 1) * (k + 2) / 2;
+  std::vector<double> h(dims3_tab(k), 0.0);
+  size_t o = 0;
+  auto put = [&](const double* src, size_t n) { memcpy(&h[o], src, sizeof(double) * n); o += n; };
+  put(tab->coef, (size_t)nb * nb);
+  put(tab->div_modal, (size_t)nbs1 * nb);
+  put(tab->vol_w, nqv);
+  put(tab->vol_D, (size_t)nqv * nbs);
+  put(tab->vol_G, (size_t)nqv * nbs * 3);
+  put(tab->fac_w, nf);
+  put(tab->fac_L, (size_t)nf * nfd);
+  put(tab->fac_D, (size_t)4 * nf * nbs);
+  put(tab->fac_len, 4);
+  const size_t NT = c->nt, NF = c->nf_facets;
+  double* d_V = nullptr;
+  int64_t *d_tet = nullptr, *d_fe = nullptr, *d_fl = nullptr;
+  int* d_slot = nullptr;
+  auto fail = [&](int code) {
+    cudaFree(d_V); cudaFree(d_tet); cudaFree(d_fe); cudaFree(d_fl); cudaFree(d_slot);
+    hdgc_destroy(c);
+    return code;
+  };
+  int rc;
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_tab, h.size() * sizeof(double)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_code, NT * 4 * sizeof(int32_t)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_piola, NT * 9 * sizeof(double)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_minv, NT * sizeof(double)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_sign, NT * sizeof(double)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_scratch, NT * nb * sizeof(double)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_prep, NT * (4 * (size_t)nqv + 4 * (size_t)nf) * sizeof(double)))) return fail(rc);
+#define SETUP3_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) \
+    return fail(hdgc_set_err(HDGC_ECUDA, "%s: %s", #x, cudaGetErrorString(e_))); } while (0)
+  SETUP3_TRY(cudaMemcpy(c->d_tab, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+  SETUP3_TRY(cudaMalloc(&d_V, sizeof(double) * 3 * c->nv));
+  SETUP3_TRY(cudaMalloc(&d_tet, sizeof(int64_t) * 4 * NT));
+  SETUP3_TRY(cudaMalloc(&d_fe, sizeof(int64_t) * 2 * NF));
+  SETUP3_TRY(cudaMalloc(&d_fl, sizeof(int64_t) * 2 * NF));
+  SETUP3_TRY(cudaMalloc(&d_slot, sizeof(int) * (NF + 2)));
+  SETUP3_TRY(cudaMemcpy(d_V, mesh->vertices, sizeof(double) * 3 * c->nv, cudaMemcpyHostToDevice));
+  SETUP3_TRY(cudaMemcpy(d_tet, mesh->elements, sizeof(int64_t) * 4 * NT, cudaMemcpyHostToDevice));
+  SETUP3_TRY(cudaMemcpy(d_fe, mesh->facet_elems, sizeof(int64_t) * 2 * NF, cudaMemcpyHostToDevice));
+  SETUP3_TRY(cudaMemcpy(d_fl, mesh->facet_local, sizeof(int64_t) * 2 * NF, cudaMemcpyHostToDevice));
+  int* d_misc = d_slot + NF;
+  SETUP3_TRY(cudaMemset(d_misc, 0, 2 * sizeof(int)));
+  {
+    const int th = 256;
+    geometry3d_kernel<<<(int)((NT + th - 1) / th), th>>>(d_V, d_tet, (int)NT, c->d_piola, c->d_minv, c->d_sign,
+                                                         d_misc + 1);
+    bflag_kernel<<<(int)((NF + th - 1) / th), th>>>(d_fe, (int)NF, d_slot);
+    scan_kernel<<<1, 1024>>>(d_slot, (int)NF, d_misc);
+    codes_kernel<<<(int)((NF + th - 1) / th), th>>>(d_fe, d_fl, d_slot, (int)NF, 4, c->d_code, d_misc + 1);
+    SETUP3_TRY(cudaGetLastError());
+  }
+  int misc[2];
+  SETUP3_TRY(cudaMemcpy(misc, d_misc, sizeof(misc), cudaMemcpyDeviceToHost));
+  if (misc[1] == 1) return fail(hdgc_set_err(HDGC_EINVAL, "degenerate tetrahedron (detJ = 0)"));
+  if (misc[1] == 2) return fail(hdgc_set_err(HDGC_EINVAL, "invalid facet_elems/facet_local entry"));
+  c->nbf = misc[0];
+  cudaFree(d_V); cudaFree(d_tet); cudaFree(d_fe); cudaFree(d_fl); cudaFree(d_slot);
+  *out = c;
+  return HDGC_OK;
+#undef SETUP3_TRY
+}
+
 extern "C" {
 
 const char* hdgc_last_error(void) { return g_err.c_str(); }
@@ -180,7 +333,8 @@ const char* hdgc_version(void) { return "hdgconv 0.1 sm_100a fp64"; }
 int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ctx** out) {
   if (!mesh || !tab || !out) return hdgc_set_err(HDGC_EINVAL, "null argument");
   *out = nullptr;
-  if (mesh->dim != 2) return hdgc_set_err(HDGC_EUNSUP, "dim=%d not supported by this build", mesh->dim);
+  if (mesh->dim == 3) return create3d(mesh, tab, out);
+  if (mesh->dim != 2) return hdgc_set_err(HDGC_EUNSUP, "dim=%d not supported (2 or 3)", mesh->dim);
   const int k = tab->k;
   if (k < 1 || k > 8) return hdgc_set_err(HDGC_EUNSUP, "order k=%d not supported (1..8)", k);
   if (tab->nqv != dims_nqv(k) || tab->nf != dims_nf(k))
@@ -273,7 +427,7 @@ int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ct
 int hdgc_destroy(hdgc_ctx* c) {
   if (!c) return HDGC_OK;
   cudaFree(c->d_tab); cudaFree(c->d_code); cudaFree(c->d_piola); cudaFree(c->d_minv);
-  cudaFree(c->d_scratch); cudaFree(c->d_scratch2); cudaFree(c->d_modal); cudaFree(c->d_prep); cudaFree(c->d_ftab); cudaFree(c->d_hu); cudaFree(c->d_hw); cudaFree(c->d_hr); cudaFree(c->d_hin);
+  cudaFree(c->d_sign); cudaFree(c->d_scratch); cudaFree(c->d_scratch2); cudaFree(c->d_modal); cudaFree(c->d_prep); cudaFree(c->d_ftab); cudaFree(c->d_hu); cudaFree(c->d_hw); cudaFree(c->d_hr); cudaFree(c->d_hin);
   delete c;
   return HDGC_OK;
 }
@@ -317,8 +471,9 @@ int hdgc_substeps(hdgc_ctx* c, const double* u, double* w, const double* inflow,
   cudaStream_t st = (cudaStream_t)stream;
   double* a = w;
   double* b = c->d_scratch;
-  if (nsteps > 0 && c->variant == 1) {
-    int rc = prep(c, u, st);    // u is frozen over the substep batch
+  if (nsteps > 0 && c->variant >= 1) {
+    // u is frozen over the substep batch: one prep per batch
+    int rc = c->variant == 2 ? prep3(c, u, st) : prep(c, u, st);
     if (rc) return rc;
   }
   for (int s = 0; s < nsteps; ++s) {
@@ -345,6 +500,7 @@ int hdgc_mass_inverse(hdgc_ctx* c, double* out, void* stream) {
 
 int hdgc_max_speed(hdgc_ctx* c, const double* u, double* out_dev, void* stream) {
   if (!c || !u || !out_dev) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (c->dim == 3) return maxspeed3(c, u, out_dev, (cudaStream_t)stream);
   HDGC_K_SWITCH(c->k, launch_maxspeed<KK>(c, u, out_dev, (cudaStream_t)stream));
 }
 
@@ -355,7 +511,7 @@ static int ensure_staging(hdgc_ctx* c, bool need_inflow) {
   if (!c->d_hw && (rc = hdgc_dev_alloc(c, (void**)&c->d_hw, vec))) return rc;
   if (!c->d_hr && (rc = hdgc_dev_alloc(c, (void**)&c->d_hr, vec))) return rc;
   if (need_inflow && !c->d_hin && c->nbf > 0 &&
-      (rc = hdgc_dev_alloc(c, (void**)&c->d_hin, sizeof(double) * (size_t)c->nbf * c->nf * 2)))
+      (rc = hdgc_dev_alloc(c, (void**)&c->d_hin, sizeof(double) * (size_t)c->nbf * c->nf * c->dim)))
     return rc;
   return HDGC_OK;
 }
@@ -370,7 +526,7 @@ int hdgc_apply_v_host(hdgc_ctx* c, const double* u, const double* w, const doubl
   CUDA_TRY(cudaMemcpyAsync(c->d_hw, w, vec, cudaMemcpyHostToDevice, st));
   const double* din = nullptr;
   if (inflow && c->nbf > 0) {
-    CUDA_TRY(cudaMemcpyAsync(c->d_hin, inflow, sizeof(double) * (size_t)c->nbf * c->nf * 2, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(c->d_hin, inflow, sizeof(double) * (size_t)c->nbf * c->nf * c->dim, cudaMemcpyHostToDevice, st));
     din = c->d_hin;
   }
   if ((rc = apply_any(c, MODE_APPLY, c->d_hu, c->d_hw, din, c->d_hr, 0.0, false, st))) return rc;
@@ -390,7 +546,7 @@ int hdgc_substeps_host(hdgc_ctx* c, const double* u, double* w, const double* in
   CUDA_TRY(cudaMemcpyAsync(c->d_hw, w, vec, cudaMemcpyHostToDevice, st));
   const double* din = nullptr;
   if (inflow && c->nbf > 0) {
-    CUDA_TRY(cudaMemcpyAsync(c->d_hin, inflow, sizeof(double) * (size_t)c->nbf * c->nf * 2, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(c->d_hin, inflow, sizeof(double) * (size_t)c->nbf * c->nf * c->dim, cudaMemcpyHostToDevice, st));
     din = c->d_hin;
   }
   if ((rc = hdgc_substeps(c, c->d_hu, c->d_hw, din, dt, nsteps, stream))) return rc;

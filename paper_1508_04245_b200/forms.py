@@ -96,6 +96,26 @@ def device_tables(k: int) -> dict:
     }
 
 
+def device_tables3(k: int) -> dict:
+    """3D (tetrahedra) tables: the same fields as device_tables, with the face
+    normal-trace basis fac_L = 2 D2_m(s_q, t_q) (dual of the face moments,
+    Gram I/2) and fac_len = 2|f| (the face Jacobian ds_hat / (ds dt))."""
+    from . import basis3d as B3
+    bdm = B3.build_bdm3_basis(k)
+    qv = B3.volume_rule3(k)
+    qf = B3.face_rule(k)
+    D, G = B3.dubiner3_values(k, qv.points, with_grads=True)
+    fD = np.stack([B3.dubiner3_values(k, B3.face_points(f, qf.points)) for f in range(4)])
+    c = np.ascontiguousarray
+    return {
+        "coef": c(bdm.coef), "div_modal": c(B3.bdm3_divergence_modal(k)),
+        "vol_w": c(qv.weights), "vol_D": c(D), "vol_G": c(G),
+        "fac_w": c(qf.weights), "fac_L": c(2.0 * B.dubiner_values(k, qf.points)),
+        "fac_D": c(fD), "fac_len": c(2.0 * B3.TET_FACE_AREAS),
+        "nqv": qv.weights.size, "nf": qf.weights.size,
+    }
+
+
 def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
@@ -121,9 +141,16 @@ class ConvectionOperator:
         lib = _lib.load()
         self.mesh = mesh
         self.k = int(k)
-        self.nb = B.nb_of(k)
-        self.nbs = B.nbs_of(k)
-        tab = device_tables(k)
+        self.dim = 3 if hasattr(mesh, "tets") else 2
+        if self.dim == 3:
+            from . import basis3d as B3
+            self.nbs = B3.nbs3_of(k)
+            self.nb = 3 * self.nbs
+            tab = device_tables3(k)
+        else:
+            self.nb = B.nb_of(k)
+            self.nbs = B.nbs_of(k)
+            tab = device_tables(k)
         self.nf = tab["nf"]
         self.nqv = tab["nqv"]
         keep = []
@@ -134,7 +161,7 @@ class ConvectionOperator:
             return _ptr(a)
 
         md = _lib.MeshDesc(
-            dim=2, n_vertices=len(mesh.vertices), n_elements=mesh.n_elements,
+            dim=self.dim, n_vertices=len(mesh.vertices), n_elements=mesh.n_elements,
             n_facets=mesh.n_facets, vertices=arr(mesh.vertices), elements=arr(mesh.triangles, np.int64),
             facet_elems=arr(mesh.facet_elems, np.int64), facet_local=arr(mesh.facet_local, np.int64),
             facet_perm=None)
@@ -143,7 +170,7 @@ class ConvectionOperator:
             vol_w=arr(tab["vol_w"]), vol_D=arr(tab["vol_D"]), vol_G=arr(tab["vol_G"]),
             fac_w=arr(tab["fac_w"]), fac_L=arr(tab["fac_L"]), fac_D=arr(tab["fac_D"]),
             fac_len=arr(tab["fac_len"]))
-        if self.k >= 3:
+        if self.k >= 3 and self.dim == 2:
             ct = B.collapsed_tables(self.k)
             td.col_n = ct["n"]
             for name in ("A", "Ad", "B", "Bd", "xi", "wa", "wy", "inv1my"):
@@ -193,7 +220,7 @@ class ConvectionOperator:
     def _inflow(self, inflow):
         if inflow is None:
             return None, None
-        t, _ = self._dev(inflow, (self.n_boundary_facets, self.nf, 2), "inflow")
+        t, _ = self._dev(inflow, (self.n_boundary_facets, self.nf, self.dim), "inflow")
         return t, C.c_void_p(t.data_ptr())
 
     # -- operators -------------------------------------------------------------

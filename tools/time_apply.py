@@ -69,5 +69,39 @@ def main():
         print(json.dumps(out[-1]))
 
 
+
+
+def main3(n=32, k=3, reps=5):
+    from paper_1508_04245_b200 import fields3d as F3, mesh3d as M3
+    m = M3.generate_cube(n)
+    vp = F3.VectorPotential(4, 5)
+    u = F3.interpolate_curl3(m, k, vp)
+    w = F3.transfer_I3_host(m, k, u)
+    op = ConvectionOperator(m, k)
+    ud, wd = torch.from_numpy(u).cuda(), torch.from_numpy(w).cuda()
+    r = torch.empty_like(wd)
+    op.apply(ud, wd, out=r)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        op.apply(ud, wd, out=r)
+    e1.record()
+    torch.cuda.synchronize()
+    ta = e0.elapsed_time(e1) * 1e-3 / reps
+    e0.record()
+    op.substeps(ud, wd, 1e-7, 20)
+    e1.record()
+    torch.cuda.synchronize()
+    ts = e0.elapsed_time(e1) * 1e-3 / 20
+    nb = 3 * (k + 1) * (k + 2) * (k + 3) // 6
+    pinned = 159720 if k == 3 else None
+    print(json.dumps(dict(dim=3, k=k, NT=m.n_elements, apply_us=ta * 1e6, substep_us=ts * 1e6,
+                          dofs_per_s=m.n_elements * nb / ts,
+                          pinned_tflops=(m.n_elements * pinned / ts / 1e12) if pinned else None)))
+
+
 if __name__ == "__main__":
-    main()
+    if "--3d" in sys.argv:
+        main3()
+    else:
+        main()
