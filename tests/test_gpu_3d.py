@@ -37,7 +37,8 @@ def test_apply3d_vs_golden(name):
     assert rel(r, g["r_ld"]) < APPLY_TOL and rel(r, g["r"]) < APPLY_TOL
     rr = op.apply(dev(g["u"]), dev(g["w_rand"]), dev(g["inflow"]))
     assert rel(rr, g["r_rand_ld"]) < APPLY_TOL
-    assert rel(op.transfer(dev(g["u"])), g["w"]) < 1e-13
+    # I = P coef: rounding scales with cond(BDM3 Vandermonde) (866 at k=3, 1.2e4 at k=4)
+    assert rel(op.transfer(dev(g["u"])), g["w"]) < max(1e-13, 1e-16 * B3.build_bdm3_basis(k).cond)
     f = np.random.default_rng(0).standard_normal(g["w"].shape)
     # I^T is the adjoint of I: <I^T f, u> = <f, I u>
     itf = op.transfer(dev(f), transpose=True).cpu().numpy()
