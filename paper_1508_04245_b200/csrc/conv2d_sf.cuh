@@ -52,23 +52,25 @@ struct SF {
   static constexpr int C_PB = C_PA + NQ;           // [NQ] w_p xi_p / (1 - y_p)
   static constexpr int C_PW = C_PB + NQ;           // [NQ] w_p
   static constexpr int C_TOTAL = C_PW + NQ;
-  // prep row: alpha | beta | gamma | s, padded to PREP_PAD doubles (16-B rows for
-  // the bulk copy; PREP_PAD = 2 mod 4 spreads the per-element rows over the banks)
+  // prep data per element: alpha | beta | gamma | s (PREP slots).  Global layout is
+  // tile-blocked and slot-major, prep[tile][slot][e] with e < EPB, so that the
+  // prep kernels write coalesced, a tile is one contiguous bulk copy, and lanes
+  // of the substep kernel read consecutive addresses (conflict-free).
   static constexpr int P_AL = 0;
   static constexpr int P_BE = NQ;
   static constexpr int P_GA = 2 * NQ;
   static constexpr int P_S = 3 * NQ;
   static constexpr int PREP = 3 * NQ + 3 * NF;
-  static constexpr int PREP_PAD = PREP + ((2 - PREP % 4) + 4) % 4;
   static constexpr int EPB = 16;                    // elements per CTA
-  static constexpr int THREADS = 2 * EPB;
-  // smem (doubles): mbarrier | prep tile [EPB][PREP_PAD] | w tile [EPB][NB] |
+  static constexpr int THREADS = 4 * EPB;            // two warps: volume | facets
+  static constexpr int PREP_TILE = PREP * 16;      // doubles per tile (EPB = 16)
+  // smem (doubles): mbarrier | prep tile [PREP][EPB] | w tile [EPB][NB] |
   //                 halo [THREADS][NBS] | fD [3][NF][NBS]
   static constexpr int SM_BAR = 0;
   static constexpr int SM_PREP = 2;
-  static constexpr int SM_W = SM_PREP + EPB * PREP_PAD;
+  static constexpr int SM_W = SM_PREP + PREP_TILE;
   static constexpr int SM_HALO = SM_W + EPB * NB;
-  static constexpr int SM_FD = SM_HALO + THREADS * NBS + ((THREADS * NBS) & 1);
+  static constexpr int SM_FD = SM_HALO + 32 * NBS + ((32 * NBS) & 1);
   static constexpr int TAB = 3 * NF * NBS;
   static constexpr int TAB_PAD = TAB + (TAB & 1);   // 16-B multiple for the bulk copy
   static constexpr int SMEM_DOUBLES = SM_FD + TAB_PAD;
@@ -121,7 +123,7 @@ prep_fused2d_kernel(const double* __restrict__ u, int nt, double* __restrict__ p
   const double* C = sf_tab<K>();
   const int T = blockIdx.x * blockDim.x + threadIdx.x;
   if (T >= nt) return;
-  double* out = prep + (size_t)T * F::PREP_PAD;
+  double* out = prep + (size_t)(T / 16) * F::PREP_TILE + (T % 16);   // slot stride 16
   double uh[NB], dv[NBS1 > 0 ? NBS1 : 1];
   {
     double x[NB];
@@ -135,7 +137,7 @@ prep_fused2d_kernel(const double* __restrict__ u, int nt, double* __restrict__ p
 #pragma unroll
         for (int l = 0; l < NE; ++l) a = fma(x[e * NE + l], CM[O_FL + q * NE + l], a);
         const double Fq = a * CM[O_FLEN + e];
-        out[F::P_S + e * NF + q] = Fq < 0.0 ? CM[O_FW + q] * Fq : 0.0;
+        out[(F::P_S + e * NF + q) * 16] = Fq < 0.0 ? CM[O_FW + q] * Fq : 0.0;
       }
     }
 #pragma unroll
@@ -180,9 +182,9 @@ prep_fused2d_kernel(const double* __restrict__ u, int nt, double* __restrict__ p
         if (i < K) dq = fma(Ai, Hd[i], dq);
       }
       const int p = b * N + a;
-      out[F::P_AL + p] = fma(C[F::C_PA + p], u0, C[F::C_PB + p] * u1);
-      out[F::P_BE + p] = C[F::C_PW + p] * u1;
-      out[F::P_GA + p] = C[F::C_PW + p] * dq;
+      out[(F::P_AL + p) * 16] = fma(C[F::C_PA + p], u0, C[F::C_PB + p] * u1);
+      out[(F::P_BE + p) * 16] = C[F::C_PW + p] * u1;
+      out[(F::P_GA + p) * 16] = C[F::C_PW + p] * dq;
     }
   }
 }
@@ -205,7 +207,7 @@ prep_points2d_kernel(const double* __restrict__ tab, const double* __restrict__ 
   const int T = (int)(gid / R);
   const int slot = (int)(gid - (long long)T * R);
   const double* C = sf_tab<K>();
-  double* out = prep + (size_t)T * F::PREP_PAD;
+  double* out = prep + (size_t)(T / 16) * F::PREP_TILE + (T % 16);   // slot stride 16
   if (slot < NQ) {
     const double* Dp = tab + D::OFF_VD + slot * NBS;
     const double* mr = modal + (size_t)T * MR;
@@ -217,23 +219,23 @@ prep_points2d_kernel(const double* __restrict__ tab, const double* __restrict__ 
       u1 = fma(__ldg(mr + NBS + m), d, u1);
       if (m < NBS1) dq = fma(__ldg(mr + NB + m), d, dq);
     }
-    out[F::P_AL + slot] = fma(C[F::C_PA + slot], u0, C[F::C_PB + slot] * u1);
-    out[F::P_BE + slot] = C[F::C_PW + slot] * u1;
-    out[F::P_GA + slot] = C[F::C_PW + slot] * dq;
+    out[(F::P_AL + slot) * 16] = fma(C[F::C_PA + slot], u0, C[F::C_PB + slot] * u1);
+    out[(F::P_BE + slot) * 16] = C[F::C_PW + slot] * u1;
+    out[(F::P_GA + slot) * 16] = C[F::C_PW + slot] * dq;
   } else {
     const int eq = slot - NQ, e = eq / NF, q = eq - e * NF;
     double a = 0.0;
 #pragma unroll
     for (int l = 0; l < NE; ++l) a = fma(__ldg(u + (size_t)T * NB + e * NE + l), __ldg(tab + D::OFF_FL + q * NE + l), a);
     const double Fq = a * __ldg(tab + D::OFF_FLEN + e);
-    out[F::P_S + eq] = Fq < 0.0 ? __ldg(tab + D::OFF_FW + q) * Fq : 0.0;
+    out[(F::P_S + eq) * 16] = Fq < 0.0 ? __ldg(tab + D::OFF_FW + q) * Fq : 0.0;
   }
 }
 
 // ---------------------------------------------------------------------------
 // per-apply / per-substep kernel
 struct SFParams {
-  const double* __restrict__ prep;    // (NT, PREP_PAD)
+  const double* __restrict__ prep;    // tile-blocked [tile][PREP][16]
   const double* __restrict__ w;       // (NT, NB)
   const double* __restrict__ inflow;  // (NBF, NF, 2) or nullptr
   const int32_t* __restrict__ code;   // (NT, 3)
@@ -295,224 +297,232 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// Two warps per CTA on one tile of EPB = 16 elements: warp 0 computes the
+// volume term, warp 1 the upwind facet term, concurrently; lane l of either
+// warp owns (element l/2, component l%2).  The facet warp leaves its partial
+// residual in shared memory (its halo buffer), the volume warp adds it and
+// runs the epilogue.  Splitting the two halves of the work halves the tile's
+// latency and keeps each warp under ~146 registers (7 CTAs = 14 warps/SM).
+#ifdef HDGC_SF_MINB
+#define HDGC_SF_MINB_OF(K) HDGC_SF_MINB
+#else
+#define HDGC_SF_MINB_OF(K) (K <= 4 ? 6 : (K <= 6 ? 4 : 2))   // register caps 170 / 256 / 255
+#endif
 template <int K, int MODE>
-__global__ void __launch_bounds__(SF<K>::THREADS)
+__global__ void __launch_bounds__(SF<K>::THREADS, HDGC_SF_MINB_OF(K))
 conv2d_sf_kernel(SFParams p) {
   using F = SF<K>;
   constexpr int N = F::N, NE = F::NE, NBS = F::NBS, NB = F::NB, NF = F::NF, EPB = F::EPB;
   extern __shared__ __align__(128) double sm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + F::SM_BAR);
-  double* s_prep = sm + F::SM_PREP;        // [EPB][PREP_PAD]
+  double* s_prep = sm + F::SM_PREP;        // [PREP][EPB]
   double* s_w = sm + F::SM_W;              // [EPB][NB]  (c-major, as in global)
-  double* s_halo = sm + F::SM_HALO;        // [THREADS][NBS]
+  double* s_halo = sm + F::SM_HALO;        // [32][NBS]: facet warp halo, then its partial r
   double* s_fD = sm + F::SM_FD;            // [3][NF][NBS]
   const double* C = sf_tab<K>();
 
   const int T0 = blockIdx.x * EPB;
   const int nel = min(EPB, p.nt - T0);
-  // ---- stage the tile with two bulk copies (one mbarrier phase)
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t bp = (uint32_t)(nel * F::PREP_PAD * sizeof(double));
+    const uint32_t bp = (uint32_t)(F::PREP_TILE * sizeof(double));
     const uint32_t bw = (uint32_t)(nel * NB * sizeof(double));
     const uint32_t bt = (uint32_t)(F::TAB_PAD * sizeof(double));
     mbar_arrive_expect_tx(bar, bp + bw + bt);
-    bulk_g2s(s_prep, p.prep + (size_t)T0 * F::PREP_PAD, bp, bar);
+    bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
     bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
     bulk_g2s(s_fD, p.ftab, bt, bar);
   }
 
-  const int le = threadIdx.x >> 1;
-  const int c = threadIdx.x & 1;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int le = lane >> 1;
+  const int c = lane & 1;
   const bool active = le < nel;
   const int T = T0 + (active ? le : 0);
-  int codes[3];
+  double* part = s_halo + lane * NBS;
+  double r[NBS];
 #pragma unroll
-  for (int ed = 0; ed < 3; ++ed) codes[ed] = active ? __ldg(p.code + (size_t)T * 3 + ed) : -1;
-  const double sc = MODE == MODE_SUBSTEP && active ? p.dt * __ldg(p.minv + T) : 0.0;
-  mbar_wait(bar, 0);
+  for (int m = 0; m < NBS; ++m) r[m] = 0.0;
 
-  const double* row = s_prep + (active ? le : 0) * F::PREP_PAD;
-  const double* wc = s_w + (active ? le : 0) * NB + c * NBS;      // w_c[m]
-  double* halo = s_halo + threadIdx.x * NBS;
-
-  // ---- prefetch (cp.async) the first out-of-tile inflow neighbour trace data
-  int halo_edge = -1;
-  if (active) {
+  if (warp == 0) {
+    // ===================== volume warp =====================
+    const double sc = MODE == MODE_SUBSTEP && active ? p.dt * __ldg(p.minv + T) : 0.0;
+    mbar_wait(bar, 0);
+    const double* row = s_prep + (active ? le : 0);        // slot j at row[j * EPB]
+    const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
+    double wo[NBS];
 #pragma unroll
-    for (int ed = 0; ed < 3; ++ed) {
-      const int code = codes[ed];
-      if (code < 0 || halo_edge >= 0) continue;
-      const int nbT = code >> 2;
-      if (nbT >= T0 && nbT < T0 + nel) continue;
-      bool any = false;
-#pragma unroll
-      for (int q = 0; q < NF; ++q) any |= row[F::P_S + ed * NF + q] != 0.0;
-      if (!any) continue;
-      halo_edge = ed;
-      const double* g = p.w + (size_t)nbT * NB + c * NBS;
-#pragma unroll
-      for (int m = 0; m < NBS; ++m) cp_async8(halo + m, g + m);
-    }
-  }
-
-  double r[NBS], wo[NBS];
-#pragma unroll
-  for (int m = 0; m < NBS; ++m) {
-    r[m] = 0.0;
-    wo[m] = wc[m];      // own w_c in registers for the volume and facet terms
-  }
-
-  // ---- volume, sum-factorised over rows b of the collapsed rule
-#ifdef HDGC_ROW_UNROLL
-  constexpr int ROW_UNROLL = HDGC_ROW_UNROLL;
-#else
-  constexpr int ROW_UNROLL = 1;   // rolled: the unrolled body overflows the i-cache (ncu: no_instruction stalls)
-#endif
-#pragma unroll ROW_UNROLL
-  for (int b = 0; b < N; ++b) {
-    const double* Bb = C + F::C_B + b * NBS;
-    const double* Bdb = C + F::C_BD + b * NBS;
-    double Hw[NE], Hwd[NE];
-#pragma unroll
-    for (int i = 0; i <= K; ++i) {
-      double sw = 0.0, swd = 0.0;
-#pragma unroll
-      for (int j = 0; j <= K - i; ++j) {
-        const int m = midx(i, j);
-        const double wv = wo[m];
-        sw = fma(wv, Bb[m], sw);
-        swd = fma(wv, Bdb[m], swd);
-      }
-      Hw[i] = sw;
-      Hwd[i] = swd;
-    }
-    const double* al = row + F::P_AL + b * N;
-    const double* be = row + F::P_BE + b * N;
-    const double* ga = row + F::P_GA + b * N;
-    double Kc[NE];
-#pragma unroll
-    for (int i = 0; i <= K; ++i) Kc[i] = 0.0;
-#pragma unroll
-    for (int a = 0; a < N; ++a) {
-      double wv = 0.0, wxi = 0.0, wyy = 0.0;
+    for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
+#pragma unroll 1
+    for (int b = 0; b < N; ++b) {
+      const double* Bb = C + F::C_B + b * NBS;
+      const double* Bdb = C + F::C_BD + b * NBS;
+      double Hw[NE], Hwd[NE];
 #pragma unroll
       for (int i = 0; i <= K; ++i) {
-        const double Ai = C[F::C_A + a * NE + i];
-        wv = fma(Ai, Hw[i], wv);
-        wxi = fma(C[F::C_AD + a * NE + i], Hw[i], wxi);
-        wyy = fma(Ai, Hwd[i], wyy);
-      }
-      const double g = fma(al[a], wxi, fma(be[a], wyy, ga[a] * wv));
+        double sw = 0.0, swd = 0.0;
 #pragma unroll
-      for (int i = 0; i <= K; ++i) Kc[i] = fma(g, C[F::C_A + a * NE + i], Kc[i]);
-    }
-#pragma unroll
-    for (int i = 0; i <= K; ++i) {
-#pragma unroll
-      for (int j = 0; j <= K - i; ++j) {
-        const int m = midx(i, j);
-        r[m] = fma(Kc[i], Bb[m], r[m]);
-      }
-    }
-  }
-
-  // ---- facets: upwind jump at inflow points only (s != 0).  Own-edge traces and
-  //      the test use compile-time constant-bank operands (ed, q unrolled); the
-  //      neighbour's edge e2 varies per thread, so its table is read from smem.
-  if (halo_edge >= 0) cp_async_wait_all();
-  const double* FD = fd_tab<K>();
-  if (active) {
-#pragma unroll
-    for (int ed = 0; ed < 3; ++ed) {
-      const double* se = row + F::P_S + ed * NF;
-      double sv[NF];
-      bool any = false;
-#pragma unroll
-      for (int q = 0; q < NF; ++q) {
-        sv[q] = se[q];
-        any |= sv[q] != 0.0;
-      }
-      if (!any) continue;
-      const int code = codes[ed];
-      double wn[NBS];
-      const double* infl = nullptr;
-      int e2 = 0;
-      if (code >= 0) {
-        const int nbT = code >> 2;
-        e2 = code & 3;
-        const double* src = (nbT >= T0 && nbT < T0 + nel) ? s_w + (nbT - T0) * NB + c * NBS
-                            : (ed == halo_edge) ? halo : nullptr;
-        if (src != nullptr) {
-#pragma unroll
-          for (int m = 0; m < NBS; ++m) wn[m] = src[m];
-        } else {
-          const double* g = p.w + (size_t)nbT * NB + c * NBS;
-#pragma unroll
-          for (int m = 0; m < NBS; ++m) wn[m] = __ldg(g + m);
+        for (int j = 0; j <= K - i; ++j) {
+          const int m = midx(i, j);
+          sw = fma(wo[m], Bb[m], sw);
+          swd = fma(wo[m], Bdb[m], swd);
         }
-      } else if (p.inflow != nullptr) {
-        infl = p.inflow + (size_t)(-1 - code) * NF * 2 + c;
+        Hw[i] = sw;
+        Hwd[i] = swd;
+      }
+      const double* al = row + (F::P_AL + b * N) * EPB;
+      const double* be = row + (F::P_BE + b * N) * EPB;
+      const double* ga = row + (F::P_GA + b * N) * EPB;
+      double Kc[NE];
+#pragma unroll
+      for (int i = 0; i <= K; ++i) Kc[i] = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        double wv = 0.0, wxi = 0.0, wyy = 0.0;
+#pragma unroll
+        for (int i = 0; i <= K; ++i) {
+          const double Ai = C[F::C_A + a * NE + i];
+          wv = fma(Ai, Hw[i], wv);
+          wxi = fma(C[F::C_AD + a * NE + i], Hw[i], wxi);
+          wyy = fma(Ai, Hwd[i], wyy);
+        }
+        const double g = fma(al[a * EPB], wxi, fma(be[a * EPB], wyy, ga[a * EPB] * wv));
+#pragma unroll
+        for (int i = 0; i <= K; ++i) Kc[i] = fma(g, C[F::C_A + a * NE + i], Kc[i]);
+      }
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+#pragma unroll
+        for (int j = 0; j <= K - i; ++j) {
+          const int m = midx(i, j);
+          r[m] = fma(Kc[i], Bb[m], r[m]);
+        }
+      }
+    }
+    asm volatile("bar.sync 1, 64;\n" ::: "memory");   // (A) facet partial r ready, in-tile w reads done
+    if (active) {
+      double* wo_s = s_w + le * NB + c * NBS;
+      if (MODE == MODE_SUBSTEP) {
+#pragma unroll
+        for (int m = 0; m < NBS; ++m) wo_s[m] = fma(-sc, r[m] + part[m], wo[m]);
       } else {
-        continue;   // boundary without inflow data: exterior = own trace
+#pragma unroll
+        for (int m = 0; m < NBS; ++m) wo_s[m] = r[m] + part[m];
       }
-      // all NF points of the edge at once: NF independent accumulation chains;
-      // outflow points carry sv[q] = 0 and contribute nothing
-      double own[NF], ext[NF];
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      bulk_s2g(p.out + (size_t)T0 * NB, s_w, (uint32_t)(nel * NB * sizeof(double)));
+      bulk_wait_read();
+    }
+  } else {
+    // ===================== facet warp =====================
+    int codes[3];
 #pragma unroll
-      for (int q = 0; q < NF; ++q) own[q] = 0.0;
+    for (int ed = 0; ed < 3; ++ed) codes[ed] = active ? __ldg(p.code + (size_t)T * 3 + ed) : -1;
+    mbar_wait(bar, 0);
+    const double* row = s_prep + (active ? le : 0);        // slot j at row[j * EPB]
+    const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
+    double* halo = part;
+    int halo_edge = -1;
+    if (active) {
 #pragma unroll
-      for (int m = 0; m < NBS; ++m) {
+      for (int ed = 0; ed < 3; ++ed) {
+        const int code = codes[ed];
+        if (code < 0 || halo_edge >= 0) continue;
+        const int nbT = code >> 2;
+        if (nbT >= T0 && nbT < T0 + nel) continue;
+        bool any = false;
 #pragma unroll
-        for (int q = 0; q < NF; ++q) own[q] = fma(wo[m], FD[(ed * NF + q) * NBS + m], own[q]);
+        for (int q = 0; q < NF; ++q) any |= row[(F::P_S + ed * NF + q) * EPB] != 0.0;
+        if (!any) continue;
+        halo_edge = ed;
+        const double* g = p.w + (size_t)nbT * NB + c * NBS;
+#pragma unroll
+        for (int m = 0; m < NBS; ++m) cp_async8(halo + m, g + m);
       }
-      if (code >= 0) {
-        const double* Dn = s_fD + e2 * NF * NBS;   // neighbour edge, reversed points
+    }
+    double wo[NBS];
 #pragma unroll
-        for (int q = 0; q < NF; ++q) ext[q] = 0.0;
+    for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
+    if (halo_edge >= 0) cp_async_wait_all();
+    const double* FD = fd_tab<K>();
+    if (active) {
+#pragma unroll
+      for (int ed = 0; ed < 3; ++ed) {
+        const double* se = row + (F::P_S + ed * NF) * EPB;
+        double sv[NF];
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < NF; ++q) {
+          sv[q] = se[q * EPB];
+          any |= sv[q] != 0.0;
+        }
+        if (!any) continue;
+        const int code = codes[ed];
+        double wn[NBS];
+        const double* infl = nullptr;
+        int e2 = 0;
+        if (code >= 0) {
+          const int nbT = code >> 2;
+          e2 = code & 3;
+          const double* src = (nbT >= T0 && nbT < T0 + nel) ? s_w + (nbT - T0) * NB + c * NBS
+                              : (ed == halo_edge) ? halo : nullptr;
+          if (src != nullptr) {
+#pragma unroll
+            for (int m = 0; m < NBS; ++m) wn[m] = src[m];
+          } else {
+            const double* g = p.w + (size_t)nbT * NB + c * NBS;
+#pragma unroll
+            for (int m = 0; m < NBS; ++m) wn[m] = __ldg(g + m);
+          }
+        } else if (p.inflow != nullptr) {
+          infl = p.inflow + (size_t)(-1 - code) * NF * 2 + c;
+        } else {
+          continue;   // boundary without inflow data: exterior = own trace
+        }
+        double own[NF], ext[NF];
+#pragma unroll
+        for (int q = 0; q < NF; ++q) own[q] = 0.0;
 #pragma unroll
         for (int m = 0; m < NBS; ++m) {
 #pragma unroll
-          for (int q = 0; q < NF; ++q) ext[q] = fma(wn[m], Dn[(NF - 1 - q) * NBS + m], ext[q]);
+          for (int q = 0; q < NF; ++q) own[q] = fma(wo[m], FD[(ed * NF + q) * NBS + m], own[q]);
         }
-      } else {
+        if (code >= 0) {
+          const double* Dn = s_fD + e2 * NF * NBS;   // neighbour edge, reversed points
 #pragma unroll
-        for (int q = 0; q < NF; ++q) ext[q] = sv[q] != 0.0 ? __ldg(infl + 2 * q) : own[q];
-      }
+          for (int q = 0; q < NF; ++q) ext[q] = 0.0;
 #pragma unroll
-      for (int q = 0; q < NF; ++q) own[q] = sv[q] * (ext[q] - own[q]);
+          for (int m = 0; m < NBS; ++m) {
 #pragma unroll
-      for (int m = 0; m < NBS; ++m) {
-        double acc = r[m];
+            for (int q = 0; q < NF; ++q) ext[q] = fma(wn[m], Dn[(NF - 1 - q) * NBS + m], ext[q]);
+          }
+        } else {
 #pragma unroll
-        for (int q = 0; q < NF; ++q) acc = fma(own[q], FD[(ed * NF + q) * NBS + m], acc);
-        r[m] = acc;
+          for (int q = 0; q < NF; ++q) ext[q] = sv[q] != 0.0 ? __ldg(infl + 2 * q) : own[q];
+        }
+#pragma unroll
+        for (int q = 0; q < NF; ++q) own[q] = sv[q] * (ext[q] - own[q]);
+#pragma unroll
+        for (int m = 0; m < NBS; ++m) {
+          double acc = r[m];
+#pragma unroll
+          for (int q = 0; q < NF; ++q) acc = fma(own[q], FD[(ed * NF + q) * NBS + m], acc);
+          r[m] = acc;
+        }
       }
     }
-  }
-
-  // ---- epilogue: outputs into the w tile (in-tile neighbour reads are done),
-  //      then one bulk store of the tile
-  __syncthreads();
-  if (active) {
-    double* wo = s_w + le * NB + c * NBS;
-    if (MODE == MODE_SUBSTEP) {
+    __syncwarp();          // halo reads of all lanes done before the partials overwrite it
 #pragma unroll
-      for (int m = 0; m < NBS; ++m) wo[m] = fma(-sc, r[m], wo[m]);
-    } else {
-#pragma unroll
-      for (int m = 0; m < NBS; ++m) wo[m] = r[m];
-    }
-  }
-  fence_proxy_async();   // generic-proxy smem writes -> visible to the bulk copy
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    bulk_s2g(p.out + (size_t)T0 * NB, s_w, (uint32_t)(nel * NB * sizeof(double)));
-    bulk_wait_read();
+    for (int m = 0; m < NBS; ++m) part[m] = r[m];
+    asm volatile("bar.sync 1, 64;\n" ::: "memory");   // (A)
   }
 }
 

@@ -260,7 +260,9 @@ int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& 
     int rc = hdgc_dev_alloc(c, (void**)&c->d_ftab, sizeof(double) * F::TAB_PAD);
     if (rc) return rc;
     CUDA_TRY(cudaMemcpy(c->d_ftab, ft.data(), sizeof(double) * F::TAB_PAD, cudaMemcpyHostToDevice));
-    rc = hdgc_dev_alloc(c, (void**)&c->d_prep, sizeof(double) * (size_t)c->nt * F::PREP_PAD);
+    rc = hdgc_dev_alloc(c, (void**)&c->d_prep, sizeof(double) * (size_t)((c->nt + 15) / 16) * F::PREP_TILE);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemset(c->d_prep, 0, sizeof(double) * (size_t)((c->nt + 15) / 16) * F::PREP_TILE));
     if (rc) return rc;
     c->variant = 1;
     return HDGC_OK;
