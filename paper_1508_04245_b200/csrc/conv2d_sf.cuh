@@ -71,8 +71,9 @@ struct SF {
   static constexpr int SM_W = SM_PREP + PREP_TILE;
   static constexpr int SM_HALO = SM_W + EPB * NB;
   static constexpr int SM_FD = SM_HALO + 32 * NBS + ((32 * NBS) & 1);
-  static constexpr int TAB = 3 * NF * NBS;
-  static constexpr int TAB_PAD = TAB + (TAB & 1);   // 16-B multiple for the bulk copy
+  static constexpr int QP = NF + (NF & 1);          // facet points padded to 16 B
+  static constexpr int TAB = 3 * NBS * QP;          // smem facet table, transposed [edge][m][QP]
+  static constexpr int TAB_PAD = TAB;               // 16-B multiple for the bulk copy
   static constexpr int SMEM_DOUBLES = SM_FD + TAB_PAD;
 };
 
@@ -358,7 +359,12 @@ conv2d_sf_kernel(SFParams p) {
     double wo[NBS];
 #pragma unroll
     for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
-#pragma unroll 1
+#ifdef HDGC_ROW_UNROLL
+    constexpr int ROW_UNROLL = HDGC_ROW_UNROLL;
+#else
+    constexpr int ROW_UNROLL = 1;
+#endif
+#pragma unroll ROW_UNROLL
     for (int b = 0; b < N; ++b) {
       const double* Bb = C + F::C_B + b * NBS;
       const double* Bdb = C + F::C_BD + b * NBS;
@@ -452,71 +458,72 @@ conv2d_sf_kernel(SFParams p) {
 #pragma unroll
     for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
     if (halo_edge >= 0) cp_async_wait_all();
-    const double* FD = fd_tab<K>();
+    __shared__ double zero_row[NBS];
+    for (int m = lane; m < NBS; m += 32) zero_row[m] = 0.0;
+    __syncwarp();
+    // inflow-edge work list: every lane walks only its own inflow edges, so the
+    // warp runs max_lane(#inflow edges) iterations (usually 2) instead of all
+    // three with idle lanes.  Edge tables: smem, transposed [edge][m][QP].
+    unsigned emask = 0;
     if (active) {
 #pragma unroll
       for (int ed = 0; ed < 3; ++ed) {
-        const double* se = row + (F::P_S + ed * NF) * EPB;
-        double sv[NF];
         bool any = false;
 #pragma unroll
-        for (int q = 0; q < NF; ++q) {
-          sv[q] = se[q * EPB];
-          any |= sv[q] != 0.0;
-        }
-        if (!any) continue;
-        const int code = codes[ed];
-        double wn[NBS];
-        const double* infl = nullptr;
-        int e2 = 0;
-        if (code >= 0) {
-          const int nbT = code >> 2;
-          e2 = code & 3;
-          const double* src = (nbT >= T0 && nbT < T0 + nel) ? s_w + (nbT - T0) * NB + c * NBS
-                              : (ed == halo_edge) ? halo : nullptr;
-          if (src != nullptr) {
+        for (int q = 0; q < NF; ++q) any |= row[(F::P_S + ed * NF + q) * EPB] != 0.0;
+        const bool has_ext = codes[ed] >= 0 || p.inflow != nullptr;   // else exterior = own trace
+        if (any && has_ext) emask |= 1u << ed;
+      }
+    }
+    const int nmine = __popc(emask);
+    const int nmax = __reduce_max_sync(0xffffffffu, (unsigned)nmine);
+    constexpr int QP = F::QP;
+#pragma unroll 1
+    for (int j = 0; j < nmax; ++j) {
+      const bool on = j < nmine;
+      const int ed = on ? __ffs(emask) - 1 : 0;
+      if (on) emask &= emask - 1;
+      const int code = ed == 0 ? codes[0] : (ed == 1 ? codes[1] : codes[2]);
+      double sv[NF];
 #pragma unroll
-            for (int m = 0; m < NBS; ++m) wn[m] = src[m];
-          } else {
-            const double* g = p.w + (size_t)nbT * NB + c * NBS;
+      for (int q = 0; q < NF; ++q) sv[q] = on ? row[(F::P_S + ed * NF + q) * EPB] : 0.0;
+      // neighbour coefficients: CTA tile or halo (smem), rarely global (generic loads)
+      const double* src = zero_row;     // zeros: no neighbour term
+      const double* infl = nullptr;
+      int e2 = 0;
+      if (on && code >= 0) {
+        const int nbT = code >> 2;
+        e2 = code & 3;
+        src = (nbT >= T0 && nbT < T0 + nel) ? s_w + (nbT - T0) * NB + c * NBS
+              : (ed == halo_edge) ? halo : p.w + (size_t)nbT * NB + c * NBS;
+      } else if (on) {
+        infl = p.inflow + (size_t)(-1 - code) * NF * 2 + c;
+      }
+      const double* De = s_fD + ed * NBS * QP;
+      const double* Dn = s_fD + e2 * NBS * QP;
+      // jump[q] = w_ext(q) - w_own(q); the neighbour traverses the edge backwards
+      double jump[NF];
 #pragma unroll
-            for (int m = 0; m < NBS; ++m) wn[m] = __ldg(g + m);
-          }
-        } else if (p.inflow != nullptr) {
-          infl = p.inflow + (size_t)(-1 - code) * NF * 2 + c;
-        } else {
-          continue;   // boundary without inflow data: exterior = own trace
-        }
-        double own[NF], ext[NF];
+      for (int q = 0; q < NF; ++q) jump[q] = 0.0;
+#pragma unroll 3
+      for (int m = 0; m < NBS; ++m) {
+        const double wn = src[m], wm = s_w[(active ? le : 0) * NB + c * NBS + m];
 #pragma unroll
-        for (int q = 0; q < NF; ++q) own[q] = 0.0;
+        for (int q = 0; q < NF; ++q) jump[q] = fma(wn, Dn[m * QP + (NF - 1 - q)], fma(-wm, De[m * QP + q], jump[q]));
+      }
+      if (infl != nullptr) {
 #pragma unroll
-        for (int m = 0; m < NBS; ++m) {
+        for (int q = 0; q < NF; ++q) jump[q] += sv[q] != 0.0 ? __ldg(infl + 2 * q) : 0.0;
+      }
+      double own[NF];
 #pragma unroll
-          for (int q = 0; q < NF; ++q) own[q] = fma(wo[m], FD[(ed * NF + q) * NBS + m], own[q]);
-        }
-        if (code >= 0) {
-          const double* Dn = s_fD + e2 * NF * NBS;   // neighbour edge, reversed points
+      for (int q = 0; q < NF; ++q) own[q] = sv[q] * jump[q];
 #pragma unroll
-          for (int q = 0; q < NF; ++q) ext[q] = 0.0;
+      for (int m = 0; m < NBS; ++m) {
+        double acc = r[m];
 #pragma unroll
-          for (int m = 0; m < NBS; ++m) {
-#pragma unroll
-            for (int q = 0; q < NF; ++q) ext[q] = fma(wn[m], Dn[(NF - 1 - q) * NBS + m], ext[q]);
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < NF; ++q) ext[q] = sv[q] != 0.0 ? __ldg(infl + 2 * q) : own[q];
-        }
-#pragma unroll
-        for (int q = 0; q < NF; ++q) own[q] = sv[q] * (ext[q] - own[q]);
-#pragma unroll
-        for (int m = 0; m < NBS; ++m) {
-          double acc = r[m];
-#pragma unroll
-          for (int q = 0; q < NF; ++q) acc = fma(own[q], FD[(ed * NF + q) * NBS + m], acc);
-          r[m] = acc;
-        }
+        for (int q = 0; q < NF; ++q) acc = fma(own[q], De[m * QP + q], acc);   // m must stay unrolled: r[] in registers
+        r[m] = acc;
       }
     }
     __syncwarp();          // halo reads of all lanes done before the partials overwrite it

@@ -242,9 +242,13 @@ int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& 
         h[F::C_PW + b * F::N + a] = wp;
       }
     CUDA_TRY(cudaMemcpyToSymbol(c_sf, h.data(), sizeof(double) * F::C_TOTAL));
+    CUDA_TRY(cudaMemcpyToSymbol(c_fd, &packed[D::OFF_FD], sizeof(double) * 3 * F::NF * F::NBS));
+    // smem copy for the substep kernel: transposed [edge][m][QP] (QP = NF padded)
     std::vector<double> ft(F::TAB_PAD, 0.0);
-    memcpy(&ft[0], &packed[D::OFF_FD], sizeof(double) * 3 * F::NF * F::NBS);
-    CUDA_TRY(cudaMemcpyToSymbol(c_fd, ft.data(), sizeof(double) * F::TAB));
+    for (int e = 0; e < 3; ++e)
+      for (int q = 0; q < F::NF; ++q)
+        for (int m = 0; m < F::NBS; ++m)
+          ft[(e * F::NBS + m) * F::QP + q] = packed[D::OFF_FD + (e * F::NF + q) * F::NBS + m];
 #if HDGC_CM_FUSED
     {
       // [coef ; divm] | fL | fw | flen for the fused prep kernel
