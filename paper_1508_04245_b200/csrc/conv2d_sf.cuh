@@ -63,6 +63,12 @@ struct SF {
   static constexpr int PREP = 3 * NQ + 3 * NF;
   static constexpr int EPB = 16;                    // elements per CTA
   static constexpr int THREADS = 4 * EPB;            // two warps: volume | facets
+#ifdef HDGC_FACET_ROWS
+  static constexpr int FACET_ROWS = HDGC_FACET_ROWS;
+#else
+  // volume rows taken by the facet warp to balance the two warps (measured per k)
+  static constexpr int FACET_ROWS = K == 5 ? 1 : (K == 7 ? 2 : 0);
+#endif
   static constexpr int PREP_TILE = PREP * 16;      // doubles per tile (EPB = 16)
   // smem (doubles): mbarrier | prep tile [PREP][EPB] | w tile [EPB][NB] |
   //                 halo [THREADS][NBS] | fD [3][NF][NBS]
@@ -298,6 +304,67 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// Volume rows [b0, b1) of the collapsed rule for one (element, component):
+// per row b, H_i = sum_j w_ij B_ij(b), H'_i (dB/dy), then values/derivatives at
+// the n points via A_i(xi_a), g = alpha d_xi w + beta d_y|xi w + gamma w, and
+// the test back into r.  wc: w_c in smem; row: the element's prep column.
+template <int K>
+__device__ __forceinline__ void sf_rows(const double* wc, const double* row, int b0, int b1,
+                                        double (&r)[SF<K>::NBS]) {
+  using F = SF<K>;
+  constexpr int N = F::N, NE = F::NE, NBS = F::NBS, EPB = F::EPB;
+  const double* C = sf_tab<K>();
+  double wo[NBS];
+#pragma unroll
+  for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
+#pragma unroll 1
+  for (int b = b0; b < b1; ++b) {
+    const double* Bb = C + F::C_B + b * NBS;
+    const double* Bdb = C + F::C_BD + b * NBS;
+    double Hw[NE], Hwd[NE];
+#pragma unroll
+    for (int i = 0; i <= K; ++i) {
+      double sw = 0.0, swd = 0.0;
+#pragma unroll
+      for (int j = 0; j <= K - i; ++j) {
+        const int m = midx(i, j);
+        sw = fma(wo[m], Bb[m], sw);
+        swd = fma(wo[m], Bdb[m], swd);
+      }
+      Hw[i] = sw;
+      Hwd[i] = swd;
+    }
+    const double* al = row + (F::P_AL + b * N) * EPB;
+    const double* be = row + (F::P_BE + b * N) * EPB;
+    const double* ga = row + (F::P_GA + b * N) * EPB;
+    double Kc[NE];
+#pragma unroll
+    for (int i = 0; i <= K; ++i) Kc[i] = 0.0;
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      double wv = 0.0, wxi = 0.0, wyy = 0.0;
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        const double Ai = C[F::C_A + a * NE + i];
+        wv = fma(Ai, Hw[i], wv);
+        wxi = fma(C[F::C_AD + a * NE + i], Hw[i], wxi);
+        wyy = fma(Ai, Hwd[i], wyy);
+      }
+      const double g = fma(al[a * EPB], wxi, fma(be[a * EPB], wyy, ga[a * EPB] * wv));
+#pragma unroll
+      for (int i = 0; i <= K; ++i) Kc[i] = fma(g, C[F::C_A + a * NE + i], Kc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i <= K; ++i) {
+#pragma unroll
+      for (int j = 0; j <= K - i; ++j) {
+        const int m = midx(i, j);
+        r[m] = fma(Kc[i], Bb[m], r[m]);
+      }
+    }
+  }
+}
+
 // Two warps per CTA on one tile of EPB = 16 elements: warp 0 computes the
 // volume term, warp 1 the upwind facet term, concurrently; lane l of either
 // warp owns (element l/2, component l%2).  The facet warp leaves its partial
@@ -359,57 +426,7 @@ conv2d_sf_kernel(SFParams p) {
     double wo[NBS];
 #pragma unroll
     for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
-#ifdef HDGC_ROW_UNROLL
-    constexpr int ROW_UNROLL = HDGC_ROW_UNROLL;
-#else
-    constexpr int ROW_UNROLL = 1;
-#endif
-#pragma unroll ROW_UNROLL
-    for (int b = 0; b < N; ++b) {
-      const double* Bb = C + F::C_B + b * NBS;
-      const double* Bdb = C + F::C_BD + b * NBS;
-      double Hw[NE], Hwd[NE];
-#pragma unroll
-      for (int i = 0; i <= K; ++i) {
-        double sw = 0.0, swd = 0.0;
-#pragma unroll
-        for (int j = 0; j <= K - i; ++j) {
-          const int m = midx(i, j);
-          sw = fma(wo[m], Bb[m], sw);
-          swd = fma(wo[m], Bdb[m], swd);
-        }
-        Hw[i] = sw;
-        Hwd[i] = swd;
-      }
-      const double* al = row + (F::P_AL + b * N) * EPB;
-      const double* be = row + (F::P_BE + b * N) * EPB;
-      const double* ga = row + (F::P_GA + b * N) * EPB;
-      double Kc[NE];
-#pragma unroll
-      for (int i = 0; i <= K; ++i) Kc[i] = 0.0;
-#pragma unroll
-      for (int a = 0; a < N; ++a) {
-        double wv = 0.0, wxi = 0.0, wyy = 0.0;
-#pragma unroll
-        for (int i = 0; i <= K; ++i) {
-          const double Ai = C[F::C_A + a * NE + i];
-          wv = fma(Ai, Hw[i], wv);
-          wxi = fma(C[F::C_AD + a * NE + i], Hw[i], wxi);
-          wyy = fma(Ai, Hwd[i], wyy);
-        }
-        const double g = fma(al[a * EPB], wxi, fma(be[a * EPB], wyy, ga[a * EPB] * wv));
-#pragma unroll
-        for (int i = 0; i <= K; ++i) Kc[i] = fma(g, C[F::C_A + a * NE + i], Kc[i]);
-      }
-#pragma unroll
-      for (int i = 0; i <= K; ++i) {
-#pragma unroll
-        for (int j = 0; j <= K - i; ++j) {
-          const int m = midx(i, j);
-          r[m] = fma(Kc[i], Bb[m], r[m]);
-        }
-      }
-    }
+    sf_rows<K>(wc, row, 0, N - F::FACET_ROWS, r);
     asm volatile("bar.sync 1, 64;\n" ::: "memory");   // (A) facet partial r ready, in-tile w reads done
     if (active) {
       double* wo_s = s_w + le * NB + c * NBS;
@@ -526,6 +543,8 @@ conv2d_sf_kernel(SFParams p) {
         r[m] = acc;
       }
     }
+    // balance: the facet warp also takes the last FACET_ROWS volume rows
+    if (F::FACET_ROWS > 0) sf_rows<K>(wc, row, N - F::FACET_ROWS, N, r);
     __syncwarp();          // halo reads of all lanes done before the partials overwrite it
 #pragma unroll
     for (int m = 0; m < NBS; ++m) part[m] = r[m];
