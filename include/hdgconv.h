@@ -92,6 +92,12 @@ typedef struct {
   const double* col_wa;      /* (n) */
   const double* col_wy;      /* (n) */
   const double* col_inv1my;  /* (n) 1/(1-y_b) */
+  /* 3D sum-factorisation (tets): D_ijl(a,b,c) = A_i(a) B_ij(b) C_ijl(c), see
+   * basis3d.collapsed_tables3; col_A/col_Ad/col_B/col_Bd hold the a- and
+   * b-factors, col_B indexed by the pair (i,j) */
+  const double* col_C;       /* (n, nbs) */
+  const double* col_Cd;      /* (n, nbs) d/dc */
+  const double* col_pf;      /* (n^3, 5) per point: w/t1, w a/t1, w/t2, w b/t2, w */
 } hdgc_tables_desc;
 
 typedef struct {

@@ -39,7 +39,7 @@ class TablesDesc(C.Structure):
         ("fac_D", C.c_void_p), ("fac_len", C.c_void_p),
         ("col_n", C.c_int32), ("col_A", C.c_void_p), ("col_Ad", C.c_void_p), ("col_B", C.c_void_p),
         ("col_Bd", C.c_void_p), ("col_xi", C.c_void_p), ("col_wa", C.c_void_p), ("col_wy", C.c_void_p),
-        ("col_inv1my", C.c_void_p),
+        ("col_inv1my", C.c_void_p), ("col_C", C.c_void_p), ("col_Cd", C.c_void_p), ("col_pf", C.c_void_p),
     ]
 
 

@@ -304,3 +304,55 @@ def bdm3_divergence_modal(k: int) -> np.ndarray:
     q = quad_tet(2 * k)
     D = dubiner3_values(k - 1, q.points)
     return 6.0 * (D * q.weights[:, None]).T @ build_bdm3_basis(k).divergence(q.points)
+
+
+def midx3(i: int, j: int, l: int) -> int:
+    """Position of mode (i, j, l) in dubiner3_index order."""
+    d = i + j + l
+    return d * (d + 1) * (d + 2) // 6 + l * (d + 1) - l * (l - 1) // 2 + j
+
+
+@lru_cache(maxsize=None)
+def collapsed_tables3(k: int) -> dict:
+    """Sum-factorisation tables of the tet Dubiner modes on volume_rule3(k)
+    (collapsed coordinates x = a(1-b)(1-c), y = b(1-c), z = c):
+        D_ijl(a, b, c) = A_i(a) B_ij(b) C_ijl(c),
+        A_i = P_i(2a-1),  B_ij = (1-b)^i P_j^(2i+1,0)(2b-1),
+        C_ijl = c_ijl (1-c)^(i+j) P_l^(2i+2j+2,0)(2c-1),
+    with derivatives Ad, Bd, Cd.  B/Bd columns are indexed by the pair
+    (i, j) in 2D Dubiner order ((i+j)(i+j+1)/2 + j), C/Cd columns by the mode.
+    Returns also the 1D points a, b, c, and per-point t1 = (1-b)(1-c),
+    t2 = 1-c are implied by them."""
+    n = (3 * k + 1) // 2
+    q = volume_rule3(k)
+    assert q.n1 == n
+    xa, _ = roots_legendre(n)
+    a = 0.5 * (xa + 1.0)
+    b, _ = _gj01(n, 1.0)
+    c, _ = _gj01(n, 2.0)
+    norms = _dub3_norms(k)
+    A = np.zeros((n, k + 1))
+    Ad = np.zeros((n, k + 1))
+    lv, ld = B2._legendre_pd(k, a)
+    sc = np.sqrt(2.0 * np.arange(k + 1) + 1.0)
+    A[:] = lv / sc
+    Ad[:] = ld / sc
+    npair = (k + 1) * (k + 2) // 2
+    Bt = np.zeros((n, npair))
+    Bd = np.zeros((n, npair))
+    for i in range(k + 1):
+        P, dP = B2._jacobi_a0(k - i, 2.0 * i + 1.0, 2.0 * b - 1.0)
+        for j in range(k - i + 1):
+            pi = (i + j) * (i + j + 1) // 2 + j
+            Bt[:, pi] = (1 - b) ** i * P[j]
+            Bd[:, pi] = (-i * (1 - b) ** (i - 1) if i else 0.0) * P[j] + (1 - b) ** i * 2.0 * dP[j]
+    nbs = nbs3_of(k)
+    Ct = np.zeros((n, nbs))
+    Cd = np.zeros((n, nbs))
+    for (i, j, l) in dubiner3_index(k):
+        m = midx3(i, j, l)
+        P, dP = B2._jacobi_a0(l, 2.0 * (i + j) + 2.0, 2.0 * c - 1.0)
+        e = i + j
+        Ct[:, m] = norms[m] * (1 - c) ** e * P[l]
+        Cd[:, m] = norms[m] * ((-e * (1 - c) ** (e - 1) if e else 0.0) * P[l] + (1 - c) ** e * 2.0 * dP[l])
+    return {"n": n, "A": A, "Ad": Ad, "B": Bt, "Bd": Bd, "C": Ct, "Cd": Cd, "a": a, "b": b, "c": c}

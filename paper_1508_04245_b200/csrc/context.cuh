@@ -62,13 +62,15 @@ template <int K> int launch3_main(hdgc_ctx* c, int mode, const double* w, const 
                                   double dt, cudaStream_t st);
 template <int K> int launch3_transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st);
 template <int K> int launch3_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st);
+template <int K> int launch3_setup(hdgc_ctx* c, const hdgc_tables_desc* t);
 
 #define HDGC_DECLARE_ORDER3(K)                                                                     \
   extern template int launch3_prep<K>(hdgc_ctx*, const double*, cudaStream_t);                    \
   extern template int launch3_main<K>(hdgc_ctx*, int, const double*, const double*, double*, double, \
                                       cudaStream_t);                                               \
   extern template int launch3_transfer<K>(hdgc_ctx*, int, const double*, double*, cudaStream_t);  \
-  extern template int launch3_maxspeed<K>(hdgc_ctx*, const double*, double*, cudaStream_t);
+  extern template int launch3_maxspeed<K>(hdgc_ctx*, const double*, double*, cudaStream_t);      \
+  extern template int launch3_setup<K>(hdgc_ctx*, const hdgc_tables_desc*);
 
 #define HDGC_DECLARE_ORDER(K)                                                                      \
   extern template int launch_elem<K>(hdgc_ctx*, int, const double*, const double*, const double*,  \

@@ -39,10 +39,39 @@ struct Dims3 {
   static constexpr int OFF_FD = OFF_FL + NF * NFD;                   // [4][NF][NBS]
   static constexpr int OFF_FLEN = OFF_FD + 4 * NF * NBS;             // [4]
   static constexpr int TAB = OFF_FLEN + 4;
-  static constexpr int PREP = 4 * NQ + 4 * NF;
+  static constexpr int PREP = 4 * NQ + 4 * NF + 1;                   // + inflow-face bitmask slot
+  static constexpr int NFP = NF + (NF & 1);                          // face points padded (smem table)
+  static constexpr int RTAB = 4 * NFD * NBS;                         // face trace maps R[f][n][m]
+  static constexpr int SMEM = (RTAB + 2 * NBS * 96) * 8;             // + own / neighbour w columns
   static constexpr int EPB = 32;                                     // elements per CTA
   static constexpr int THREADS = 3 * EPB;                            // one warp per component
 };
+
+// sum-factorisation tables (constant bank of the order compiled in this TU):
+// D_ijl(a,b,c) = A_i(a) B_ij(b) C_ijl(c) on the collapsed n^3 rule
+template <int K>
+struct SF3 {
+  static constexpr int N = (3 * K + 1) / 2;
+  static constexpr int NE = K + 1;
+  static constexpr int NPAIR = (K + 1) * (K + 2) / 2;
+  static constexpr int NBS = (K + 1) * (K + 2) * (K + 3) / 6;
+  static constexpr int NQ = N * N * N;
+  static constexpr int C_A = 0, C_AD = C_A + N * NE, C_B = C_AD + N * NE, C_BD = C_B + N * NPAIR;
+  static constexpr int C_C = C_BD + N * NPAIR, C_CD = C_C + N * NBS, C_PF = C_CD + N * NBS;
+  static constexpr int NF = K == 1 ? 6 : ((3 * K + 3) / 2) * ((3 * K + 3) / 2);
+  static constexpr int NFD = (K + 1) * (K + 2) / 2;
+  static constexpr int C_D2 = C_PF + NQ * 5;                         // [NF][NFD] face modes at face points
+  static constexpr int C_TOTAL = C_D2 + NF * NFD;
+};
+
+__host__ __device__ constexpr int midx3(int i, int j, int l) {
+  return (i + j + l) * (i + j + l + 1) * (i + j + l + 2) / 6 + l * (i + j + l + 1) - l * (l - 1) / 2 + j;
+}
+__host__ __device__ constexpr int pidx(int i, int j) { return (i + j) * (i + j + 1) / 2 + j; }
+
+#ifdef HDGC_ORDER3
+__constant__ double c_sf3d[SF3<HDGC_ORDER3>::C_TOTAL];
+#endif
 
 inline int dims3_nq(int k) { const int n = (3 * k + 1) / 2; return n * n * n; }
 inline int dims3_nf(int k) {
@@ -60,6 +89,10 @@ __global__ void geometry3d_kernel(const double* __restrict__ V, const int64_t* _
                                   double* __restrict__ piola, double* __restrict__ minv,
                                   double* __restrict__ sgn, int* __restrict__ bad);
 
+#ifdef HDGC_ORDER3   // kernels: only in the per-order translation units
+#ifndef HDGC_3D_MINB
+#define HDGC_3D_MINB 2
+#endif
 struct Prep3Params {
   const double* __restrict__ tab;
   const double* __restrict__ u;
@@ -81,7 +114,9 @@ prep3d_kernel(Prep3Params p) {
   double x[NB];
 #pragma unroll
   for (int j = 0; j < NB; ++j) x[j] = __ldg(p.u + (size_t)T * NB + j);
-  // inflow weights from the face dofs (first 4*NFD dofs, face-major)
+  // inflow weights from the face dofs (first 4*NFD dofs, face-major) and the
+  // bitmask of faces with at least one inflow point
+  unsigned fmask = 0;
 #pragma unroll 1
   for (int f = 0; f < 4; ++f) {
     const double len = __ldg(tab + D::OFF_FLEN + f);
@@ -92,8 +127,10 @@ prep3d_kernel(Prep3Params p) {
       for (int m = 0; m < NFD; ++m) a = fma(x[f * NFD + m], __ldg(tab + D::OFF_FL + q * NFD + m), a);
       const double F = sg * a * len;
       p.prep[(size_t)(4 * NQ + f * NF + q) * nt + T] = F < 0.0 ? __ldg(tab + D::OFF_FW + q) * F : 0.0;
+      if (F < 0.0) fmask |= 1u << f;
     }
   }
+  p.prep[(size_t)(4 * NQ + 4 * NF) * nt + T] = (double)fmask;
   double uh[NB];
 #pragma unroll 1
   for (int i = 0; i < NB; ++i) {
@@ -122,16 +159,19 @@ prep3d_kernel(Prep3Params p) {
       a2 = fma(uh[2 * NBS + m], d, a2);
       if (m < NBS1) dq = fma(dv[m], d, dq);
     }
-    const double wq = sg * __ldg(tab + D::OFF_VW + q);
-    p.prep[(size_t)q * nt + T] = wq * a0;
-    p.prep[(size_t)(NQ + q) * nt + T] = wq * a1;
-    p.prep[(size_t)(2 * NQ + q) * nt + T] = wq * a2;
-    p.prep[(size_t)(3 * NQ + q) * nt + T] = wq * dq;
+    // flux-form coefficients in collapsed coordinates (chain rule of the Duffy map):
+    // g = alpha w_a + beta w_b + gamma w_c + delta w
+    const double* pf = c_sf3d + SF3<K>::C_PF + q * 5;
+    p.prep[(size_t)q * nt + T] = sg * fma(pf[0], a0, pf[1] * (a1 + a2));
+    p.prep[(size_t)(NQ + q) * nt + T] = sg * fma(pf[2], a1, pf[3] * a2);
+    p.prep[(size_t)(2 * NQ + q) * nt + T] = sg * pf[4] * a2;
+    p.prep[(size_t)(3 * NQ + q) * nt + T] = sg * pf[4] * dq;
   }
 }
 
 struct Conv3Params {
   const double* __restrict__ tab;
+  const double* __restrict__ rtab;    // face trace maps R[4][NFD][NBS]
   const double* __restrict__ prep;    // point-major SoA (PREP, NT)
   const double* __restrict__ w;       // (NT, NB)
   const double* __restrict__ inflow;  // (NBF, NF, 3) or nullptr
@@ -145,85 +185,185 @@ struct Conv3Params {
 // one thread per (element, component); warp w of the CTA = component w of 32
 // consecutive elements, so prep reads are coalesced and tables are uniform
 template <int K, int MODE>
-__global__ void __launch_bounds__(96)
+__global__ void __launch_bounds__(96, HDGC_3D_MINB)
 conv3d_kernel(Conv3Params p) {
   using D = Dims3<K>;
   constexpr int NB = D::NB, NBS = D::NBS, NQ = D::NQ, NF = D::NF;
   const int c = threadIdx.x / D::EPB;
-  const int T = blockIdx.x * D::EPB + (threadIdx.x % D::EPB);
-  if (T >= p.nt) return;
+  const int T0 = blockIdx.x * D::EPB + (threadIdx.x % D::EPB);
+  const bool active = T0 < p.nt;
+  const int T = active ? T0 : p.nt - 1;
   const double* tab = p.tab;
   const size_t nt = (size_t)p.nt;
+  // smem: face trace maps R[4][NFD][NBS] and per-thread w_c / neighbour columns
+  extern __shared__ __align__(16) double sm3[];
+  double* s_R = sm3;                     // [4][NFD][NBS]
+  double* s_wo = sm3 + D::RTAB;          // [NBS][96]
+  double* s_wn = s_wo + NBS * 96;        // [NBS][96]
+  for (int i = threadIdx.x; i < D::RTAB; i += blockDim.x) s_R[i] = __ldg(p.rtab + i);
   double wo[NBS], r[NBS];
 #pragma unroll
   for (int m = 0; m < NBS; ++m) {
     wo[m] = __ldg(p.w + (size_t)T * NB + c * NBS + m);
+    s_wo[m * 96 + threadIdx.x] = wo[m];
     r[m] = 0.0;
   }
-  // ---- volume
+  __syncthreads();
+  // ---- volume, sum-factorised over the collapsed rule (c outer, b, a inner):
+  //   G_ij(c) = sum_l w_ijl C_ijl(c),  H_i(b,c) = sum_j G_ij(c) B_ij(b),
+  //   w(a,b,c) = sum_i A_i(a) H_i(b,c)  (and the a-, b-, c-derivatives),
+  //   g = alpha w_a + beta w_b + gamma w_c + delta w, then the transpose chain.
+  {
+    using S = SF3<K>;
+    constexpr int N = S::N, NE = S::NE, NPAIR = S::NPAIR;
+    const double* Cs = c_sf3d;
 #pragma unroll 1
-  for (int q = 0; q < NQ; ++q) {
-    const double* Dq = tab + D::OFF_VD + q * NBS;
-    const double* Gq = tab + D::OFF_VG + q * NBS * 3;
-    double v = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+    for (int ic = 0; ic < N; ++ic) {
+      const double* Cc = Cs + S::C_C + ic * NBS;
+      const double* Ccd = Cs + S::C_CD + ic * NBS;
+      double G[NPAIR], Gc[NPAIR], K2[NPAIR];
 #pragma unroll
-    for (int m = 0; m < NBS; ++m) {
-      const double wm = wo[m];
-      v = fma(wm, __ldg(Dq + m), v);
-      gx = fma(wm, __ldg(Gq + 3 * m), gx);
-      gy = fma(wm, __ldg(Gq + 3 * m + 1), gy);
-      gz = fma(wm, __ldg(Gq + 3 * m + 2), gz);
-    }
-    const double ax = __ldg(p.prep + (size_t)q * nt + T);
-    const double ay = __ldg(p.prep + (size_t)(NQ + q) * nt + T);
-    const double az = __ldg(p.prep + (size_t)(2 * NQ + q) * nt + T);
-    const double ga = __ldg(p.prep + (size_t)(3 * NQ + q) * nt + T);
-    const double g = fma(ax, gx, fma(ay, gy, fma(az, gz, ga * v)));
+      for (int i = 0; i <= K; ++i)
 #pragma unroll
-    for (int m = 0; m < NBS; ++m) r[m] = fma(g, __ldg(Dq + m), r[m]);
-  }
-  // ---- faces: upwind jump at inflow points
+        for (int j = 0; j <= K - i; ++j) {
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int l = 0; l <= K - i - j; ++l) {
+            const int m = midx3(i, j, l);
+            s0 = fma(wo[m], Cc[m], s0);
+            s1 = fma(wo[m], Ccd[m], s1);
+          }
+          G[pidx(i, j)] = s0;
+          Gc[pidx(i, j)] = s1;
+          K2[pidx(i, j)] = 0.0;
+        }
 #pragma unroll 1
-  for (int f = 0; f < 4; ++f) {
-    const double* sf = p.prep + (size_t)(4 * NQ + f * NF) * nt + T;
-    bool any = false;
-#pragma unroll 1
-    for (int q = 0; q < NF; ++q) any |= __ldg(sf + (size_t)q * nt) != 0.0;
-    if (!any) continue;
-    const int code = __ldg(p.code + (size_t)T * 4 + f);
-    double wn[NBS];
-    int f2 = 0;
-    const double* infl = nullptr;
-    if (code >= 0) {
-      const double* g = p.w + (size_t)(code >> 2) * NB + c * NBS;
-      f2 = code & 3;
+      for (int ib = 0; ib < N; ++ib) {
+        const double* Bb = Cs + S::C_B + ib * NPAIR;
+        const double* Bbd = Cs + S::C_BD + ib * NPAIR;
+        double H[NE], Hb[NE], Hc[NE], K1[NE];
 #pragma unroll
-      for (int m = 0; m < NBS; ++m) wn[m] = __ldg(g + m);
-    } else if (p.inflow != nullptr) {
-      infl = p.inflow + (size_t)(-1 - code) * NF * 3 + c;
-    } else {
-      continue;
-    }
-    const double* Df = tab + D::OFF_FD + f * NF * NBS;
-    const double* Dn = tab + D::OFF_FD + f2 * NF * NBS;
-#pragma unroll 1
-    for (int q = 0; q < NF; ++q) {
-      const double sq = __ldg(sf + (size_t)q * nt);
-      if (sq == 0.0) continue;
-      double own = 0.0, ext = 0.0;
+        for (int i = 0; i <= K; ++i) {
+          double h = 0.0, hb = 0.0, hc = 0.0;
 #pragma unroll
-      for (int m = 0; m < NBS; ++m) own = fma(wo[m], __ldg(Df + q * NBS + m), own);
-      if (code >= 0) {
+          for (int j = 0; j <= K - i; ++j) {
+            const int pp = pidx(i, j);
+            h = fma(G[pp], Bb[pp], h);
+            hb = fma(G[pp], Bbd[pp], hb);
+            hc = fma(Gc[pp], Bb[pp], hc);
+          }
+          H[i] = h; Hb[i] = hb; Hc[i] = hc; K1[i] = 0.0;
+        }
+        const size_t q0 = (size_t)(ic * N + ib) * N;
 #pragma unroll
-        for (int m = 0; m < NBS; ++m) ext = fma(wn[m], __ldg(Dn + q * NBS + m), ext);
-      } else {
-        ext = __ldg(infl + 3 * q);
+        for (int ia = 0; ia < N; ++ia) {
+          double v = 0.0, va = 0.0, vb = 0.0, vc = 0.0;
+#pragma unroll
+          for (int i = 0; i <= K; ++i) {
+            const double Ai = Cs[S::C_A + ia * NE + i];
+            v = fma(Ai, H[i], v);
+            va = fma(Cs[S::C_AD + ia * NE + i], H[i], va);
+            vb = fma(Ai, Hb[i], vb);
+            vc = fma(Ai, Hc[i], vc);
+          }
+          const size_t q = q0 + ia;
+          const double al = __ldg(p.prep + q * nt + T);
+          const double be = __ldg(p.prep + (NQ + q) * nt + T);
+          const double ga = __ldg(p.prep + (2 * NQ + q) * nt + T);
+          const double de = __ldg(p.prep + (3 * NQ + q) * nt + T);
+          const double g = fma(al, va, fma(be, vb, fma(ga, vc, de * v)));
+#pragma unroll
+          for (int i = 0; i <= K; ++i) K1[i] = fma(g, Cs[S::C_A + ia * NE + i], K1[i]);
+        }
+#pragma unroll
+        for (int i = 0; i <= K; ++i)
+#pragma unroll
+          for (int j = 0; j <= K - i; ++j) K2[pidx(i, j)] = fma(K1[i], Bb[pidx(i, j)], K2[pidx(i, j)]);
       }
-      const double s = sq * (ext - own);
 #pragma unroll
-      for (int m = 0; m < NBS; ++m) r[m] = fma(s, __ldg(Df + q * NBS + m), r[m]);
+      for (int i = 0; i <= K; ++i)
+#pragma unroll
+        for (int j = 0; j <= K - i; ++j)
+#pragma unroll
+          for (int l = 0; l <= K - i - j; ++l) {
+            const int m = midx3(i, j, l);
+            r[m] = fma(K2[pidx(i, j)], Cc[m], r[m]);
+          }
     }
   }
+  // ---- faces: per-lane work list of inflow faces (the warp runs max_lane(count)
+  //      iterations).  Traces are handled in the face's own P_k basis: the
+  //      trace of a tet mode on face f is D_m(x_f(s,t)) = sum_n R_f[n][m] D2_n(s,t)
+  //      exactly, so the jump coefficients are d = R_f2 w_nbr - R_f w_own (NFD
+  //      numbers instead of NF point values), the jump at point q is
+  //      sum_n d_n D2_n(q), and the test folds back through R_f^T.  Point q of
+  //      the owner is point q of the neighbour (sorted tet vertices).
+  {
+    using S = SF3<K>;
+    constexpr int NFD = D::NFD;
+    const double* D2 = c_sf3d + S::C_D2;
+    unsigned fm = active ? (unsigned)__ldg(p.prep + (size_t)(4 * NQ + 4 * NF) * nt + T) : 0u;
+    if (p.inflow == nullptr) {
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+        if (active && __ldg(p.code + (size_t)T * 4 + f) < 0) fm &= ~(1u << f);   // exterior = own trace
+    }
+    const int nmine = __popc(fm);
+    const int nmax = __reduce_max_sync(0xffffffffu, (unsigned)nmine);
+#pragma unroll 1
+    for (int j = 0; j < nmax; ++j) {
+      const bool on = j < nmine;
+      const int f = on ? __ffs(fm) - 1 : 0;
+      if (on) fm &= fm - 1;
+      const int code = on ? __ldg(p.code + (size_t)T * 4 + f) : -1;
+      int f2 = 0;
+      const double* infl = nullptr;
+      if (code >= 0) {
+        const double* g = p.w + (size_t)(code >> 2) * NB + c * NBS;
+        f2 = code & 3;
+#pragma unroll
+        for (int m = 0; m < NBS; ++m) s_wn[m * 96 + threadIdx.x] = __ldg(g + m);
+      } else {
+#pragma unroll
+        for (int m = 0; m < NBS; ++m) s_wn[m * 96 + threadIdx.x] = 0.0;
+        if (on) infl = p.inflow + (size_t)(-1 - code) * NF * 3 + c;
+      }
+      const double* Rf = s_R + f * NFD * NBS;
+      const double* Rn = s_R + f2 * NFD * NBS;
+      double dl[NFD];
+#pragma unroll
+      for (int n = 0; n < NFD; ++n) dl[n] = 0.0;
+#pragma unroll 4
+      for (int m = 0; m < NBS; ++m) {
+        const double wm = s_wo[m * 96 + threadIdx.x], wnm = s_wn[m * 96 + threadIdx.x];
+#pragma unroll
+        for (int n = 0; n < NFD; ++n) dl[n] = fma(wnm, Rn[n * NBS + m], fma(-wm, Rf[n * NBS + m], dl[n]));
+      }
+      double rho[NFD];
+#pragma unroll
+      for (int n = 0; n < NFD; ++n) rho[n] = 0.0;
+      const double* sf = p.prep + (size_t)(4 * NQ + f * NF) * nt + T;
+#pragma unroll 2
+      for (int q = 0; q < NF; ++q) {
+        const double sq = on ? __ldg(sf + (size_t)q * nt) : 0.0;
+        double J = 0.0;
+#pragma unroll
+        for (int n = 0; n < NFD; ++n) J = fma(dl[n], D2[q * NFD + n], J);
+        if (infl != nullptr && sq != 0.0) J += __ldg(infl + 3 * q);
+        const double sj = sq * J;
+#pragma unroll
+        for (int n = 0; n < NFD; ++n) rho[n] = fma(sj, D2[q * NFD + n], rho[n]);
+      }
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) {
+        double acc = r[m];
+#pragma unroll
+        for (int n = 0; n < NFD; ++n) acc = fma(Rf[n * NBS + m], rho[n], acc);
+        r[m] = acc;
+      }
+    }
+  }
+  if (!active) return;
   double* og = p.out + (size_t)T * NB + c * NBS;
   if (MODE == MODE_SUBSTEP) {
     const double sc = p.dt * __ldg(p.minv + T);
@@ -322,5 +462,7 @@ maxspeed3d_kernel(const double* __restrict__ tab, const double* __restrict__ pio
   for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
 }
+
+#endif  // HDGC_ORDER3
 
 }  // namespace hdgc

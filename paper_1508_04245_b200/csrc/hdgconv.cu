@@ -229,6 +229,7 @@ static int main3(hdgc_ctx* c, int mode, const double* w, const double* inflow, d
 static int transfer3(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st) {
   HDGC_K3_SWITCH(c->k, launch3_transfer<KK>(c, dir, in, out, st));
 }
+static int setup3(hdgc_ctx* c, const hdgc_tables_desc* t) { HDGC_K3_SWITCH(c->k, launch3_setup<KK>(c, t)); }
 static int maxspeed3(hdgc_ctx* c, const double* u, double* out, cudaStream_t st) {
   HDGC_K3_SWITCH(c->k, launch3_maxspeed<KK>(c, u, out, st));
 }
@@ -290,7 +291,7 @@ static int create3d(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdg
   if ((rc = hdgc_dev_alloc(c, (void**)&c->d_minv, NT * sizeof(double)))) return fail(rc);
   if ((rc = hdgc_dev_alloc(c, (void**)&c->d_sign, NT * sizeof(double)))) return fail(rc);
   if ((rc = hdgc_dev_alloc(c, (void**)&c->d_scratch, NT * nb * sizeof(double)))) return fail(rc);
-  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_prep, NT * (4 * (size_t)nqv + 4 * (size_t)nf) * sizeof(double)))) return fail(rc);
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_prep, NT * (4 * (size_t)nqv + 4 * (size_t)nf + 1) * sizeof(double)))) return fail(rc);
 #define SETUP3_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) \
     return fail(hdgc_set_err(HDGC_ECUDA, "%s: %s", #x, cudaGetErrorString(e_))); } while (0)
   SETUP3_TRY(cudaMemcpy(c->d_tab, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -319,6 +320,7 @@ static int create3d(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdg
   if (misc[1] == 1) return fail(hdgc_set_err(HDGC_EINVAL, "degenerate tetrahedron (detJ = 0)"));
   if (misc[1] == 2) return fail(hdgc_set_err(HDGC_EINVAL, "invalid facet_elems/facet_local entry"));
   c->nbf = misc[0];
+  if ((rc = setup3(c, tab))) return fail(rc);
   cudaFree(d_V); cudaFree(d_tet); cudaFree(d_fe); cudaFree(d_fl); cudaFree(d_slot);
   *out = c;
   return HDGC_OK;

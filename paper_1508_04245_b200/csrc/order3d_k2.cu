@@ -1,4 +1,5 @@
-// 3D (tetrahedra) kernels and launchers for order k=2.
+// 3D (tetrahedra) kernels and launchers for order k=2 (own constant-bank tables).
+#define HDGC_ORDER3 2
 #include "order3d_ops.cuh"
 
 HDGC_INSTANTIATE_ORDER3(2)

@@ -1,11 +1,48 @@
 // order3d_ops.cuh — per-order launchers of the 3D kernels (included by order3d_k<K>.cu).
 #pragma once
+#include <cstring>
+#include <vector>
+
 #include "context.cuh"
 #include "conv3d.cuh"
 
 namespace hdgc {
 
 static inline unsigned grid3_for(long long work, int threads) { return (unsigned)((work + threads - 1) / threads); }
+
+// upload the sum-factorisation tables of this order (constant bank)
+template <int K>
+int launch3_setup(hdgc_ctx* c, const hdgc_tables_desc* t) {
+  using S = SF3<K>;
+  if (t->col_n != S::N || !t->col_A || !t->col_Ad || !t->col_B || !t->col_Bd || !t->col_C || !t->col_Cd ||
+      !t->col_pf)
+    return hdgc_set_err(HDGC_EINVAL, "3D collapsed tables missing or n=%d != %d", t->col_n, S::N);
+  std::vector<double> h(S::C_TOTAL);
+  memcpy(&h[S::C_A], t->col_A, sizeof(double) * S::N * S::NE);
+  memcpy(&h[S::C_AD], t->col_Ad, sizeof(double) * S::N * S::NE);
+  memcpy(&h[S::C_B], t->col_B, sizeof(double) * S::N * S::NPAIR);
+  memcpy(&h[S::C_BD], t->col_Bd, sizeof(double) * S::N * S::NPAIR);
+  memcpy(&h[S::C_C], t->col_C, sizeof(double) * S::N * S::NBS);
+  memcpy(&h[S::C_CD], t->col_Cd, sizeof(double) * S::N * S::NBS);
+  memcpy(&h[S::C_PF], t->col_pf, sizeof(double) * S::NQ * 5);
+  // face modes at the face points: D2 = fac_L / 2 (fac_L is the normal-trace basis 2 D2)
+  for (int i = 0; i < S::NF * S::NFD; ++i) h[S::C_D2 + i] = 0.5 * t->fac_L[i];
+  CUDA_TRY(cudaMemcpyToSymbol(c_sf3d, h.data(), sizeof(double) * S::C_TOTAL));
+  // face trace maps R_f[n][m] = 2 sum_q w_q D_m(x_f(q)) D2_n(q)  (exact: degree 2k <= 3k+1)
+  std::vector<double> R((size_t)4 * S::NFD * S::NBS, 0.0);
+  for (int f = 0; f < 4; ++f)
+    for (int n = 0; n < S::NFD; ++n)
+      for (int m = 0; m < S::NBS; ++m) {
+        double a = 0.0;
+        for (int q = 0; q < S::NF; ++q)
+          a += t->fac_w[q] * t->fac_D[((size_t)f * S::NF + q) * S::NBS + m] * t->fac_L[q * S::NFD + n];
+        R[((size_t)f * S::NFD + n) * S::NBS + m] = a;   // 2 * w * D * D2 = w * D * fac_L
+      }
+  int rc = hdgc_dev_alloc(c, (void**)&c->d_ftab, sizeof(double) * R.size());
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpy(c->d_ftab, R.data(), sizeof(double) * R.size(), cudaMemcpyHostToDevice));
+  return HDGC_OK;
+}
 
 template <int K>
 int launch3_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
@@ -25,6 +62,7 @@ int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, d
                  cudaStream_t st) {
   Conv3Params p;
   p.tab = c->d_tab;
+  p.rtab = c->d_ftab;
   p.prep = c->d_prep;
   p.w = w;
   p.inflow = inflow;
@@ -34,8 +72,14 @@ int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, d
   p.dt = dt;
   p.nt = c->nt;
   const unsigned blocks = grid3_for(c->nt, Dims3<K>::EPB);
-  if (mode == MODE_SUBSTEP) conv3d_kernel<K, MODE_SUBSTEP><<<blocks, Dims3<K>::THREADS, 0, st>>>(p);
-  else conv3d_kernel<K, MODE_APPLY><<<blocks, Dims3<K>::THREADS, 0, st>>>(p);
+  constexpr int smem = Dims3<K>::SMEM;
+  auto launch = [&](auto kern) -> int {
+    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<blocks, Dims3<K>::THREADS, smem, st>>>(p);
+    return HDGC_OK;
+  };
+  int rc = mode == MODE_SUBSTEP ? launch(conv3d_kernel<K, MODE_SUBSTEP>) : launch(conv3d_kernel<K, MODE_APPLY>);
+  if (rc) return rc;
   CUDA_TRY(cudaGetLastError());
   return HDGC_OK;
 }
@@ -66,4 +110,5 @@ int launch3_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st)
   template int launch3_main<K>(hdgc_ctx*, int, const double*, const double*, double*, double, cudaStream_t); \
   template int launch3_transfer<K>(hdgc_ctx*, int, const double*, double*, cudaStream_t);           \
   template int launch3_maxspeed<K>(hdgc_ctx*, const double*, double*, cudaStream_t);                \
+  template int launch3_setup<K>(hdgc_ctx*, const hdgc_tables_desc*);                               \
   }

@@ -113,7 +113,27 @@ def device_tables3(k: int) -> dict:
         "fac_w": c(qf.weights), "fac_L": c(2.0 * B.dubiner_values(k, qf.points)),
         "fac_D": c(fD), "fac_len": c(2.0 * B3.TET_FACE_AREAS),
         "nqv": qv.weights.size, "nf": qf.weights.size,
+        "col3": _collapsed3(k),
     }
+
+
+def _collapsed3(k: int) -> dict:
+    """Sum-factorisation tables for the 3D kernel (basis3d.collapsed_tables3)
+    plus the per-point factors of the flux-form coefficients
+    alpha = w (u_x + a (u_y + u_z)) / t1, beta = w (u_y + b u_z) / t2, gamma = w u_z,
+    with t1 = (1-b)(1-c), t2 = 1-c (chain rule of the collapsed map)."""
+    from . import basis3d as B3
+    t = B3.collapsed_tables3(k)
+    q = B3.volume_rule3(k)
+    n = t["n"]
+    C3, B3_, A3 = np.meshgrid(t["c"], t["b"], t["a"], indexing="ij")   # point order c, b, a
+    t1 = ((1 - B3_) * (1 - C3)).ravel()
+    t2 = (1 - C3).ravel()
+    a, b, w = A3.ravel(), B3_.ravel(), q.weights
+    pf = np.stack([w / t1, w * a / t1, w / t2, w * b / t2, w], axis=1)
+    c = np.ascontiguousarray
+    return {"n": n, "A": c(t["A"]), "Ad": c(t["Ad"]), "B": c(t["B"]), "Bd": c(t["Bd"]),
+            "C": c(t["C"]), "Cd": c(t["Cd"]), "pf": c(pf)}
 
 
 def _ptr(a: np.ndarray):
@@ -174,6 +194,11 @@ class ConvectionOperator:
             ct = B.collapsed_tables(self.k)
             td.col_n = ct["n"]
             for name in ("A", "Ad", "B", "Bd", "xi", "wa", "wy", "inv1my"):
+                setattr(td, "col_" + name, arr(ct[name]))
+        if self.dim == 3:
+            ct = tab["col3"]
+            td.col_n = ct["n"]
+            for name in ("A", "Ad", "B", "Bd", "C", "Cd", "pf"):
                 setattr(td, "col_" + name, arr(ct[name]))
         torch = _torch()
         if not torch.cuda.is_available():
