@@ -267,10 +267,13 @@ def main():
     flops, byts = pinned_work(K_ORDER)
     peak, peak_src = fp64_peak()
     achieved = NT * flops / k_s / 1e12
-    traffic = None
+    traffic = None     # dram read + write bytes per launch of the substep kernel (ncu --set full)
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_substep_r01.json")) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+        with open(os.path.join(ROOT, "profiles", "ncu_substep_k4_r01.json")) as fh:
+            nc = json.load(fh)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        traffic = sum(float(nc[k]["value"]) * scale[nc[k]["unit"]]
+                      for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     except Exception:
         pass
     cpu = None
