@@ -77,9 +77,10 @@ struct SF {
   static constexpr int SM_W = SM_PREP + PREP_TILE;
   static constexpr int SM_HALO = SM_W + EPB * NB;
   static constexpr int SM_FD = SM_HALO + 32 * NBS + ((32 * NBS) & 1);
-  static constexpr int QP = NF + (NF & 1);          // facet points padded to 16 B
-  static constexpr int TAB = 3 * NBS * QP;          // smem facet table, transposed [edge][m][QP]
-  static constexpr int TAB_PAD = TAB;               // 16-B multiple for the bulk copy
+  // smem edge trace maps R[3][NE][NBS], per-edge stride odd (bank spread across lanes)
+  static constexpr int RSTR = (NE * NBS) | 1;
+  static constexpr int TAB = 3 * NF * NBS;          // constant-bank facet table size (fD)
+  static constexpr int TAB_PAD = (3 * RSTR + 1) & ~1; // smem R table, 16-B multiple for the bulk copy
   static constexpr int SMEM_DOUBLES = SM_FD + TAB_PAD;
 };
 
@@ -91,6 +92,7 @@ struct SF {
 #if HDGC_ORDER >= 3
 __constant__ double c_sf[SF<HDGC_ORDER>::C_TOTAL];
 __constant__ double c_fd[SF<HDGC_ORDER>::TAB];   // Dubiner traces fD[3][NF][NBS]
+__constant__ double c_fl[SF<HDGC_ORDER>::NF * SF<HDGC_ORDER>::NE];   // Legendre at facet points
 // fused prep (k <= 6): [coef ; divm] (NB + NBS1 rows x NB) | fL (NF x NE) | fw (NF) | flen (3)
 #define HDGC_CM_FUSED (HDGC_ORDER <= 6)
 #if HDGC_CM_FUSED
@@ -102,6 +104,7 @@ __constant__ double c_cm[1];
 #else
 __constant__ double c_sf[1];
 __constant__ double c_fd[1];
+__constant__ double c_fl[1];
 #define HDGC_CM_FUSED 0
 __constant__ double c_cm[1];
 #endif
@@ -109,6 +112,10 @@ __constant__ double c_cm[1];
 template <int K> __device__ __forceinline__ const double* sf_tab() {
   static_assert(K == HDGC_ORDER, "sum-factorisation tables are per translation unit");
   return c_sf;
+}
+template <int K> __device__ __forceinline__ const double* fl_tab() {
+  static_assert(K == HDGC_ORDER, "facet tables are per translation unit");
+  return c_fl;
 }
 template <int K> __device__ __forceinline__ const double* fd_tab() {
   static_assert(K == HDGC_ORDER, "facet tables are per translation unit");
@@ -386,7 +393,7 @@ conv2d_sf_kernel(SFParams p) {
   double* s_prep = sm + F::SM_PREP;        // [PREP][EPB]
   double* s_w = sm + F::SM_W;              // [EPB][NB]  (c-major, as in global)
   double* s_halo = sm + F::SM_HALO;        // [32][NBS]: facet warp halo, then its partial r
-  double* s_fD = sm + F::SM_FD;            // [3][NF][NBS]
+  double* s_fD = sm + F::SM_FD;            // edge trace maps [3][RSTR]
   const double* C = sf_tab<K>();
 
   const int T0 = blockIdx.x * EPB;
@@ -494,16 +501,19 @@ conv2d_sf_kernel(SFParams p) {
     }
     const int nmine = __popc(emask);
     const int nmax = __reduce_max_sync(0xffffffffu, (unsigned)nmine);
-    constexpr int QP = F::QP;
+    // Jumps in the edge's own P_k basis: the trace of a Dubiner mode on edge e is
+    // D_m(x_e(t)) = sum_l R_e[l][m] L_l(t) exactly (orthonormal Legendre), the
+    // neighbour's trace at t' = 1 - t has coefficients (-1)^l (R_e2 w_nbr)_l,
+    // so the jump coefficients are d_l = (-1)^l (R_e2 w_nbr)_l - (R_e w_own)_l,
+    // the jump at point q is sum_l d_l L_l(t_q), and the test folds back
+    // through R_e^T.  R from smem (per-lane edge), L from the constant bank.
+    const double* FL = fl_tab<K>();
 #pragma unroll 1
     for (int j = 0; j < nmax; ++j) {
       const bool on = j < nmine;
       const int ed = on ? __ffs(emask) - 1 : 0;
       if (on) emask &= emask - 1;
       const int code = ed == 0 ? codes[0] : (ed == 1 ? codes[1] : codes[2]);
-      double sv[NF];
-#pragma unroll
-      for (int q = 0; q < NF; ++q) sv[q] = on ? row[(F::P_S + ed * NF + q) * EPB] : 0.0;
       // neighbour coefficients: CTA tile or halo (smem), rarely global (generic loads)
       const double* src = zero_row;     // zeros: no neighbour term
       const double* infl = nullptr;
@@ -516,30 +526,39 @@ conv2d_sf_kernel(SFParams p) {
       } else if (on) {
         infl = p.inflow + (size_t)(-1 - code) * NF * 2 + c;
       }
-      const double* De = s_fD + ed * NBS * QP;
-      const double* Dn = s_fD + e2 * NBS * QP;
-      // jump[q] = w_ext(q) - w_own(q); the neighbour traverses the edge backwards
-      double jump[NF];
+      const double* Re = s_fD + ed * F::RSTR;
+      const double* Rn = s_fD + e2 * F::RSTR;
+      double dl[NE];
 #pragma unroll
-      for (int q = 0; q < NF; ++q) jump[q] = 0.0;
+      for (int l = 0; l < NE; ++l) dl[l] = 0.0;
 #pragma unroll 3
       for (int m = 0; m < NBS; ++m) {
-        const double wn = src[m], wm = s_w[(active ? le : 0) * NB + c * NBS + m];
+        const double wn = src[m], wm = wc[m];
 #pragma unroll
-        for (int q = 0; q < NF; ++q) jump[q] = fma(wn, Dn[m * QP + (NF - 1 - q)], fma(-wm, De[m * QP + q], jump[q]));
+        for (int l = 0; l < NE; ++l) {
+          const double tn = (l & 1) ? -wn : wn;
+          dl[l] = fma(tn, Rn[l * NBS + m], fma(-wm, Re[l * NBS + m], dl[l]));
+        }
       }
-      if (infl != nullptr) {
+      double rho[NE];
 #pragma unroll
-        for (int q = 0; q < NF; ++q) jump[q] += sv[q] != 0.0 ? __ldg(infl + 2 * q) : 0.0;
+      for (int l = 0; l < NE; ++l) rho[l] = 0.0;
+#pragma unroll
+      for (int q = 0; q < NF; ++q) {
+        const double sq = on ? row[(F::P_S + ed * NF + q) * EPB] : 0.0;
+        double J = 0.0;
+#pragma unroll
+        for (int l = 0; l < NE; ++l) J = fma(dl[l], FL[q * NE + l], J);
+        if (infl != nullptr && sq != 0.0) J += __ldg(infl + 2 * q);
+        const double sj = sq * J;
+#pragma unroll
+        for (int l = 0; l < NE; ++l) rho[l] = fma(sj, FL[q * NE + l], rho[l]);
       }
-      double own[NF];
-#pragma unroll
-      for (int q = 0; q < NF; ++q) own[q] = sv[q] * jump[q];
 #pragma unroll
       for (int m = 0; m < NBS; ++m) {
         double acc = r[m];
 #pragma unroll
-        for (int q = 0; q < NF; ++q) acc = fma(own[q], De[m * QP + q], acc);   // m must stay unrolled: r[] in registers
+        for (int l = 0; l < NE; ++l) acc = fma(Re[l * NBS + m], rho[l], acc);
         r[m] = acc;
       }
     }

@@ -243,12 +243,19 @@ int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& 
       }
     CUDA_TRY(cudaMemcpyToSymbol(c_sf, h.data(), sizeof(double) * F::C_TOTAL));
     CUDA_TRY(cudaMemcpyToSymbol(c_fd, &packed[D::OFF_FD], sizeof(double) * 3 * F::NF * F::NBS));
-    // smem copy for the substep kernel: transposed [edge][m][QP] (QP = NF padded)
+    CUDA_TRY(cudaMemcpyToSymbol(c_fl, &packed[D::OFF_FL], sizeof(double) * F::NF * F::NE));
+    // smem table for the substep kernel: edge trace maps
+    //   R_e[l][m] = int_0^1 D_m(x_e(t)) L_l(t) dt = sum_q w_q fD[e][q][m] L[q][l]  (exact, degree 2k)
     std::vector<double> ft(F::TAB_PAD, 0.0);
     for (int e = 0; e < 3; ++e)
-      for (int q = 0; q < F::NF; ++q)
-        for (int m = 0; m < F::NBS; ++m)
-          ft[(e * F::NBS + m) * F::QP + q] = packed[D::OFF_FD + (e * F::NF + q) * F::NBS + m];
+      for (int l = 0; l < F::NE; ++l)
+        for (int m = 0; m < F::NBS; ++m) {
+          double a = 0.0;
+          for (int q = 0; q < F::NF; ++q)
+            a += packed[D::OFF_FW + q] * packed[D::OFF_FD + (e * F::NF + q) * F::NBS + m] *
+                 packed[D::OFF_FL + q * F::NE + l];
+          ft[e * F::RSTR + l * F::NBS + m] = a;
+        }
 #if HDGC_CM_FUSED
     {
       // [coef ; divm] | fL | fw | flen for the fused prep kernel
