@@ -23,6 +23,8 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_obj")
 OUT = os.path.join(HERE, "libhdgconv.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# cuBLAS for the modal-row DGEMM of the frozen-velocity prep (same CUDA image on the GPU box)
+LIBS = ["-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
 FLAGS = ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
@@ -72,7 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         results = list(ex.map(_compile, srcs))
     objs = [o for o, _ in results]
     if _stale(OUT, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", OUT + ".tmp", *objs]
+        cmd = [nvcc(), *ARCH, "-shared", "-o", OUT + ".tmp", *objs, *LIBS]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}{res.stderr}")

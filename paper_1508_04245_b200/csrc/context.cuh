@@ -39,11 +39,15 @@ struct hdgc_ctx {
   double* d_hw = nullptr;
   double* d_hr = nullptr;
   double* d_hin = nullptr;
+  void* blas = nullptr;         // cublasHandle_t for the modal GEMM (lazily created)
   int64_t bytes = 0;
   int variant = 0;              // 0: thread-per-element (k <= 2), 1: sum-factorised (k >= 3)
 };
 
 int hdgc_dev_alloc(hdgc_ctx* c, void** p, size_t bytes);
+// c->d_modal[T][r] = sum_j M[r][j] u[T][j] for r < nr (M row-major [nr][nb] at
+// c->d_tab + off): one DGEMM over all elements on stream st.
+int hdgc_modal_gemm(hdgc_ctx* c, const double* u, int nb, int nr, size_t off, cudaStream_t st);
 
 namespace hdgc {
 // per-order operations, explicitly instantiated in order_k<K>.cu

@@ -3,7 +3,7 @@
 //
 // The convecting velocity is frozen over an apply and over a whole substep
 // batch, so everything that depends on u alone is
-// evaluated once per batch (rowmat2d_kernel + prep_points2d_kernel) into a
+// evaluated once per batch (prep_fused2d_kernel, or DGEMM + prep_rows2d_kernel) into a
 // per-element "prep row":
 //   alpha(p) = w_p (u0 + xi_p u1) / (1 - y_p),   beta(p) = w_p u1,
 //   gamma(p) = w_p div u_hat                      at the n^2 volume points,
@@ -94,7 +94,7 @@ __constant__ double c_sf[SF<HDGC_ORDER>::C_TOTAL];
 __constant__ double c_fd[SF<HDGC_ORDER>::TAB];   // Dubiner traces fD[3][NF][NBS]
 __constant__ double c_fl[SF<HDGC_ORDER>::NF * SF<HDGC_ORDER>::NE];   // Legendre at facet points
 // fused prep (k <= 6): [coef ; divm] (NB + NBS1 rows x NB) | fL (NF x NE) | fw (NF) | flen (3)
-#define HDGC_CM_FUSED (HDGC_ORDER <= 6)
+#define HDGC_CM_FUSED (HDGC_ORDER <= 4)
 #if HDGC_CM_FUSED
 __constant__ double c_cm[(SF<HDGC_ORDER>::NB + SF<HDGC_ORDER>::NBS1) * SF<HDGC_ORDER>::NB +
                          SF<HDGC_ORDER>::NF * SF<HDGC_ORDER>::NE + SF<HDGC_ORDER>::NF + 3];
@@ -123,7 +123,7 @@ template <int K> __device__ __forceinline__ const double* fd_tab() {
 }
 
 // ---------------------------------------------------------------------------
-// fused prep (k <= 6), one thread per element: modal u_hat = coef u and
+// fused prep (k <= 4), one thread per element: modal u_hat = coef u and
 // div = divm u with the matrices as constant-bank operands, then alpha/beta/
 // gamma at the n x n points by sum factorisation of the velocity (per row b:
 // H_i = sum_j u_hat_ij B_ij(b), then sum_i A_i(a) H_i), and the inflow weights.
@@ -204,45 +204,79 @@ prep_fused2d_kernel(const double* __restrict__ u, int nt, double* __restrict__ p
 }
 
 // ---------------------------------------------------------------------------
-// prep, stage 2 (stage 1 = modal u_hat | div, rowmat2d_kernel): one thread
-// per (element, slot), slot < NQ: alpha/beta/gamma at volume point p;
-// NQ <= slot < NQ + 3 NF: inflow weight s_e(q) from the raw edge dofs.
+// prep, stage 2 (stage 1 = modal rows u_hat | div u_hat by one DGEMM): one CTA
+// per tile of 16 elements, one thread per (element, collapsed row b).  The
+// tile's modal rows are staged in smem; thread (e, b) evaluates the velocity on
+// row b by sum factorisation (H_i = sum_j u_ij B_ij(b), values via A_i(xi_a))
+// and writes alpha/beta/gamma of its N points; threads with b < 3 also write
+// the inflow weights of edge b.  Writes are tile-blocked and slot-major, so
+// the 16 lanes of an element group store consecutive addresses.
 template <int K>
-__global__ void __launch_bounds__(256)
-prep_points2d_kernel(const double* __restrict__ tab, const double* __restrict__ u,
-                     const double* __restrict__ modal, int nt, double* __restrict__ prep) {
+__global__ void __launch_bounds__(16 * SF<K>::N)
+prep_rows2d_kernel(const double* __restrict__ tab, const double* __restrict__ u,
+                   const double* __restrict__ modal, int nt, double* __restrict__ prep) {
   using D = Dims<K>;
   using F = SF<K>;
-  constexpr int NB = D::NB, NBS = D::NBS, NBS1 = D::NBS1, NE = D::NE, NF = D::NF, NQ = F::NQ;
-  constexpr int R = NQ + 3 * NF;            // slots per element (pad slots untouched)
-  constexpr int MR = NB + NBS1;             // modal row length
-  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (long long)nt * R) return;
-  const int T = (int)(gid / R);
-  const int slot = (int)(gid - (long long)T * R);
+  constexpr int N = F::N, NE = F::NE, NBS = F::NBS, NB = F::NB, NBS1 = F::NBS1, NF = F::NF;
+  constexpr int NR = NB + NBS1;
+  __shared__ double s_mod[16 * NR];
+  const int T0 = blockIdx.x * 16;
+  const int nel = min(16, nt - T0);
+  for (int i = threadIdx.x; i < nel * NR; i += blockDim.x) s_mod[i] = __ldg(modal + (size_t)T0 * NR + i);
+  __syncthreads();
+  const int e = threadIdx.x & 15;
+  const int b = threadIdx.x >> 4;
+  if (e >= nel) return;
   const double* C = sf_tab<K>();
-  double* out = prep + (size_t)(T / 16) * F::PREP_TILE + (T % 16);   // slot stride 16
-  if (slot < NQ) {
-    const double* Dp = tab + D::OFF_VD + slot * NBS;
-    const double* mr = modal + (size_t)T * MR;
-    double u0 = 0.0, u1 = 0.0, dq = 0.0;
+  const double* mr = s_mod + e * NR;
+  double* out = prep + (size_t)blockIdx.x * F::PREP_TILE + e;
+  {
+    const double* Bb = C + F::C_B + b * NBS;
+    double H0[NE], H1[NE], Hd[NE];
 #pragma unroll
-    for (int m = 0; m < NBS; ++m) {
-      const double d = __ldg(Dp + m);
-      u0 = fma(__ldg(mr + m), d, u0);
-      u1 = fma(__ldg(mr + NBS + m), d, u1);
-      if (m < NBS1) dq = fma(__ldg(mr + NB + m), d, dq);
+    for (int i = 0; i <= K; ++i) {
+      double s0 = 0.0, s1 = 0.0, sd = 0.0;
+#pragma unroll
+      for (int j = 0; j <= K - i; ++j) {
+        const int m = midx(i, j);
+        s0 = fma(mr[m], Bb[m], s0);
+        s1 = fma(mr[NBS + m], Bb[m], s1);
+        if (i + j < K) sd = fma(mr[NB + m], Bb[m], sd);
+      }
+      H0[i] = s0; H1[i] = s1; Hd[i] = sd;
     }
-    out[(F::P_AL + slot) * 16] = fma(C[F::C_PA + slot], u0, C[F::C_PB + slot] * u1);
-    out[(F::P_BE + slot) * 16] = C[F::C_PW + slot] * u1;
-    out[(F::P_GA + slot) * 16] = C[F::C_PW + slot] * dq;
-  } else {
-    const int eq = slot - NQ, e = eq / NF, q = eq - e * NF;
-    double a = 0.0;
 #pragma unroll
-    for (int l = 0; l < NE; ++l) a = fma(__ldg(u + (size_t)T * NB + e * NE + l), __ldg(tab + D::OFF_FL + q * NE + l), a);
-    const double Fq = a * __ldg(tab + D::OFF_FLEN + e);
-    out[(F::P_S + eq) * 16] = Fq < 0.0 ? __ldg(tab + D::OFF_FW + q) * Fq : 0.0;
+    for (int a = 0; a < N; ++a) {
+      double u0 = 0.0, u1 = 0.0, dq = 0.0;
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        const double Ai = C[F::C_A + a * NE + i];
+        u0 = fma(Ai, H0[i], u0);
+        u1 = fma(Ai, H1[i], u1);
+        if (i < K) dq = fma(Ai, Hd[i], dq);
+      }
+      const int p = b * N + a;
+      out[(F::P_AL + p) * 16] = fma(C[F::C_PA + p], u0, C[F::C_PB + p] * u1);
+      out[(F::P_BE + p) * 16] = C[F::C_PW + p] * u1;
+      out[(F::P_GA + p) * 16] = C[F::C_PW + p] * dq;
+    }
+  }
+  if (b < 3) {
+    // inflow weights of edge b: F = |e| sum_l u[b(k+1)+l] L_l(t_q)
+    const double* ue = u + (size_t)(T0 + e) * NB + b * NE;
+    double x[NE];
+#pragma unroll
+    for (int l = 0; l < NE; ++l) x[l] = __ldg(ue + l);
+    const double len = __ldg(tab + D::OFF_FLEN + b);
+    const double* FL = fl_tab<K>();
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      double a = 0.0;
+#pragma unroll
+      for (int l = 0; l < NE; ++l) a = fma(x[l], FL[q * NE + l], a);
+      const double Fq = a * len;
+      out[(F::P_S + b * NF + q) * 16] = Fq < 0.0 ? __ldg(tab + D::OFF_FW + q) * Fq : 0.0;
+    }
   }
 }
 

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <cublas_v2.h>
+
 #include "common.cuh"
 #include "context.cuh"
 #include "conv3d.cuh"
@@ -37,6 +39,24 @@ int hdgc_dev_alloc(hdgc_ctx* c, void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes);
   if (e != cudaSuccess) return hdgc_set_err(HDGC_ENOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
   c->bytes += (int64_t)bytes;
+  return HDGC_OK;
+}
+
+// Row-major out[T][r] = sum_j M[r][j] u[T][j] is, read column-major, the
+// (nr x nt) product M^T(col) x U(col):  C = op_T(A) B with A = M viewed as
+// (nb x nr, lda nb), B = u as (nb x nt, ldb nb), C = d_modal (ldc nr).
+int hdgc_modal_gemm(hdgc_ctx* c, const double* u, int nb, int nr, size_t off, cudaStream_t st) {
+  if (!c->blas) {
+    cublasHandle_t h = nullptr;
+    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return hdgc_set_err(HDGC_ECUDA, "cublasCreate failed");
+    c->blas = h;
+  }
+  cublasHandle_t h = static_cast<cublasHandle_t>(c->blas);
+  if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return hdgc_set_err(HDGC_ECUDA, "cublasSetStream failed");
+  const double one = 1.0, zero = 0.0;
+  const cublasStatus_t s = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, nr, c->nt, nb, &one, c->d_tab + off, nb, u, nb,
+                                       &zero, c->d_modal, nr);
+  if (s != CUBLAS_STATUS_SUCCESS) return hdgc_set_err(HDGC_ECUDA, "cublasDgemm (modal rows) failed: %d", (int)s);
   return HDGC_OK;
 }
 
@@ -430,6 +450,7 @@ int hdgc_destroy(hdgc_ctx* c) {
   if (!c) return HDGC_OK;
   cudaFree(c->d_tab); cudaFree(c->d_code); cudaFree(c->d_piola); cudaFree(c->d_minv);
   cudaFree(c->d_sign); cudaFree(c->d_scratch); cudaFree(c->d_scratch2); cudaFree(c->d_modal); cudaFree(c->d_prep); cudaFree(c->d_ftab); cudaFree(c->d_hu); cudaFree(c->d_hw); cudaFree(c->d_hr); cudaFree(c->d_hin);
+  if (c->blas) cublasDestroy(static_cast<cublasHandle_t>(c->blas));
   delete c;
   return HDGC_OK;
 }

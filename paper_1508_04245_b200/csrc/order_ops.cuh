@@ -12,26 +12,6 @@ namespace hdgc {
 // small per-element matrix-vector products, one thread per (element, row):
 // no large unrolled blocks, so every order compiles in seconds.
 
-// modal velocity data: out[T][r] = sum_j M[r][j] u[T][j], M = [coef ; divm]
-// (u_hat = coef u, PB:357-378; div u_hat in the P_{k-1} Dubiner modes)
-template <int K>
-__global__ void __launch_bounds__(256)
-rowmat2d_kernel(const double* __restrict__ tab, const double* __restrict__ u, int nt,
-                double* __restrict__ out) {
-  using D = Dims<K>;
-  constexpr int NB = D::NB, R = D::NB + D::NBS1;
-  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (long long)nt * R) return;
-  const int T = (int)(gid / R);
-  const int r = (int)(gid - (long long)T * R);
-  const double* M = tab + D::OFF_COEF + (size_t)r * NB;   // coef rows then divm rows (contiguous)
-  const double* x = u + (size_t)T * NB;
-  double a = 0.0;
-#pragma unroll
-  for (int j = 0; j < NB; ++j) a = fma(__ldg(M + j), __ldg(x + j), a);
-  out[gid] = a;
-}
-
 // I (BDM -> V_h): w[c*nbs+m] = sum_d P[c][d] (coef u)[d*nbs+m]
 // I^T:            r_w[j]     = sum_{d,m} coef[d*nbs+m][j] sum_c P[c][d] r[c*nbs+m]
 // one thread per (element, output row); in and out must not alias.
@@ -151,10 +131,8 @@ int launch_transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStr
 // modal rows u_hat | div u_hat into c->d_modal
 template <int K>
 int launch_modal(hdgc_ctx* c, const double* u, cudaStream_t st) {
-  const long long work = (long long)c->nt * (Dims<K>::NB + Dims<K>::NBS1);
-  rowmat2d_kernel<K><<<grid_for(work, 256), 256, 0, st>>>(c->d_tab, u, c->nt, c->d_modal);
-  CUDA_TRY(cudaGetLastError());
-  return HDGC_OK;
+  // modal velocity rows [u_hat | div u_hat] = [coef ; divm] u (PB:357-378)
+  return hdgc_modal_gemm(c, u, Dims<K>::NB, Dims<K>::NB + Dims<K>::NBS1, Dims<K>::OFF_COEF, st);
 }
 
 template <int K>
@@ -172,15 +150,20 @@ int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st) 
 // frozen-velocity prep rows (alpha | beta | gamma | s) into c->d_prep
 template <int K>
 int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
-  if constexpr (K >= 3 && K <= 6) {
+  // k <= 4: one fused thread-per-element kernel (matrices in the constant
+  // bank) beats DGEMM + rows (k=3: 35 vs 56 us, k=4: 71 vs 91 us at 131072
+  // elements); from k = 5 the DGEMM path wins (k=5 128 vs 305 us, k=8 340 us
+  // vs 3.4 ms for the old thread-per-point stage 2).
+  if constexpr (K >= 3 && K <= 4) {
     prep_fused2d_kernel<K><<<grid_for(c->nt, 128), 128, 0, st>>>(u, c->nt, c->d_prep);
     CUDA_TRY(cudaGetLastError());
     return HDGC_OK;
-  } else if constexpr (K >= 3) {
+  }
+  if constexpr (K >= 3) {
     int rc = launch_modal<K>(c, u, st);
     if (rc) return rc;
-    const long long work = (long long)c->nt * SF<K>::PREP;
-    prep_points2d_kernel<K><<<grid_for(work, 256), 256, 0, st>>>(c->d_tab, u, c->d_modal, c->nt, c->d_prep);
+    prep_rows2d_kernel<K><<<(c->nt + 15) / 16, 16 * SF<K>::N, 0, st>>>(c->d_tab, u, c->d_modal, c->nt,
+                                                                       c->d_prep);
     CUDA_TRY(cudaGetLastError());
     return HDGC_OK;
   } else {

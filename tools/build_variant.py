@@ -27,7 +27,8 @@ def main(name, *flags):
     with cf.ThreadPoolExecutor(8) as ex:
         objs = list(ex.map(comp, sorted(glob.glob(os.path.join(CSRC, "*.cu")))))
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o",
-                           os.path.join(out, "libhdgconv.so"), *objs])
+                           os.path.join(out, "libhdgconv.so"), *objs,
+                           "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"])
     print(os.path.join(out, "libhdgconv.so"))
 
 

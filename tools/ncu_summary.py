@@ -1,0 +1,75 @@
+"""Summarise an ``ncu --set full`` report (.ncu-rep) into a small JSON of the
+metrics the roofline / DESIGN.md cite, for every launch of a kernel whose name
+contains a pattern (development tool; run here on reports brought back from
+gpurun).
+
+    python tools/ncu_summary.py gpurun_out/sub_k4.ncu-rep conv2d_sf_kernel profiles/ncu_substep_k4_r01.json
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+METRICS = [
+    "gpu__time_duration.sum",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "launch__block_size",
+    "launch__grid_size",
+    "launch__registers_per_thread",
+    "launch__shared_mem_per_block_dynamic",
+    "launch__occupancy_limit_registers",
+    "launch__occupancy_limit_shared_mem",
+    "sm__warps_active.avg.per_cycle_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_selected_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__cycles_elapsed.avg.per_second",
+]
+
+
+def main(rep, pattern, out):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                         check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    head, units = rows[0], rows[1]
+    col = {n: i for i, n in enumerate(head)}
+    launches = []
+    for r in rows[2:]:
+        if pattern not in r[col["Kernel Name"]]:
+            continue
+        d = {"kernel": r[col["Kernel Name"]]}
+        for m in METRICS:
+            if m in col:
+                d[m] = {"unit": units[col[m]], "value": r[col[m]]}
+        launches.append(d)
+    if not launches:
+        raise SystemExit(f"no launch of {pattern!r} in {rep}")
+    res = dict(launches[-1])
+    res["source"] = rep.split("/")[-1]
+    res["launches_captured"] = len(launches)
+    with open(out, "w") as fh:
+        json.dump(res, fh, indent=1)
+    print(json.dumps({k: v for k, v in res.items() if k != "kernel"})[:2000])
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:4])
