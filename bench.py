@@ -128,6 +128,33 @@ def dist_init():
     return world, rank, local
 
 
+def max_over_ranks(t: float, world: int, device: str = "cuda") -> float:
+    """Max of a per-rank time over all ranks (all_reduce MAX; identity at world 1)."""
+    if world <= 1:
+        return t
+    import torch
+    import torch.distributed as dist
+    tt = torch.tensor([t], dtype=torch.float64, device=device)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
+
+
+def replica_value(units_per_rank: float, world: int, t_max: float) -> float:
+    """Whole-job throughput of independent replicas: all ranks' units / max time."""
+    return world * units_per_rank / t_max
+
+
+def ncu_fp64_flop(nc: dict):
+    """FP64 flops per launch actually executed (ncu: 2 dfma + dmul + dadd thread ops)."""
+    try:
+        cyc = float(nc["sm__cycles_elapsed.avg"]["value"])
+        per = {k: float(nc[f"smsp__sass_thread_inst_executed_op_{k}_pred_on.sum.per_cycle_elapsed"]["value"])
+               for k in ("dfma", "dmul", "dadd")}
+        return cyc * (2 * per["dfma"] + per["dmul"] + per["dadd"])
+    except Exception:
+        return None
+
+
 def run_reference(args, world, rank):
     """CPU arm: the oracle's OpenMP C port on all host cores (rank 0 only)."""
     if rank != 0:
@@ -235,13 +262,9 @@ def main():
     clk = clocks.stop() if clocks else None
     step_s = [a.elapsed_time(b) * 1e-3 for a, b in ev]
     t_step = sum(step_s) / len(step_s)
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([t_step], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step = float(tt.item())
+    t_step = max_over_ranks(t_step, world)
     dofs_per_step = NT * nb * NSUB
-    value = world * dofs_per_step / t_step
+    value = replica_value(dofs_per_step, world, t_step)
 
     # ---- average launch duration of the dominant (substep) kernel: the step is
     # one frozen-velocity prep launch + NSUB substep launches back to back on
@@ -268,12 +291,14 @@ def main():
     peak, peak_src = fp64_peak()
     achieved = NT * flops / k_s / 1e12
     traffic = None     # dram read + write bytes per launch of the substep kernel (ncu --set full)
+    measured_flop = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_substep_k4_r01.json")) as fh:
             nc = json.load(fh)
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         traffic = sum(float(nc[k]["value"]) * scale[nc[k]["unit"]]
                       for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        measured_flop = ncu_fp64_flop(nc)
     except Exception:
         pass
     cpu = None
@@ -295,6 +320,8 @@ def main():
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
                      "algorithmic": f"pinned F(k=4)={flops} flop/element (SURVEY 8d) x {NT} elements per launch",
+                     "ncu_fp64_flop_per_launch": measured_flop,
+                     "ncu_source": "profiles/ncu_substep_k4_r01.json",
                      "hbm_frac": NT * byts / k_s / 1e9 / hbm, "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src},
         "cpu_baseline": cpu,
         "e2e": {"value": world * dofs_per_step / e2e_s, "unit": UNIT,

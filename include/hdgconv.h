@@ -48,6 +48,7 @@ extern "C" {
 #define HDGC_ECUDA (-2)    /* CUDA runtime error */
 #define HDGC_ENOMEM (-3)   /* device allocation failed */
 #define HDGC_EUNSUP (-4)   /* unsupported order / dimension */
+#define HDGC_ENOCONV (-5)  /* Richardson iteration hit max_iter (result = last iterate) */
 
 typedef struct hdgc_ctx hdgc_ctx;
 
@@ -126,6 +127,28 @@ int hdgc_apply_w(hdgc_ctx* ctx, const double* u_loc, const double* inflow, doubl
  *   w <- w - dt * (M^V)^{-1} C^V(u; w),  (M^V)^{-1} = 2/detJ per element. */
 int hdgc_substeps(hdgc_ctx* ctx, const double* u_loc, double* w_inout, const double* inflow,
                   double dt, int32_t nsteps, void* stream);
+
+/* Convection propagation Q^{t1 -> t1 + nsteps ds} (SPEC.md:429-437,
+ * timeloop.propagate_convection), device-resident:
+ *   scheme 0: forward Euler, 1: SSP-RK2 (Heun: v1 = v - ds M^-1 C(s) v,
+ *   v' = v/2 + (v1 - ds M^-1 C(s + ds) v1)/2).
+ * Convecting velocity at pseudo time s: u_cur if u_prev is NULL (frozen),
+ * else the linear extrapolation u(s) = u_cur + (s - t_cur)/(t_cur - t_prev)
+ * (u_cur - u_prev) of two stored divergence-free fields. */
+int hdgc_propagate(hdgc_ctx* ctx, const double* u_prev, const double* u_cur, double t_prev, double t_cur,
+                   double t1, double ds, int32_t nsteps, int32_t scheme, const double* inflow,
+                   double* w_inout, void* stream);
+
+/* Richardson / pseudo-time solve of v + tau (M^V)^{-1} C^V v = g (PAPER.md:671-687,
+ * SPEC.md:456-464, timeloop.pseudo_time_solve):
+ *   res_i = g - v_i - tau M^-1 C v_i,  v_{i+1} = v_i + ds res_i,
+ * stopping at the first i with ||res_i||_2 <= rho ||res_0||_2 (v_inout <- v_i,
+ * *iters = i).  Returns HDGC_ENOCONV when i reaches max_iter first (v_inout =
+ * v_max_iter).  Synchronises `stream` once per iteration to read the norm;
+ * the norm is a fixed-order (deterministic) reduction. */
+int hdgc_richardson(hdgc_ctx* ctx, const double* u_loc, const double* g, const double* inflow, double tau,
+                    double ds, double rho, int32_t max_iter, double* v_inout, int32_t* iters,
+                    double* res0, double* res_final, void* stream);
 
 /* Transfer operators: direction 0: out = I in (BDM -> V_h),
  * direction 1: out = I^T in (V_h functionals -> BDM-test layout). */

@@ -11,14 +11,18 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("HDGC_LIB", os.path.join(HERE, "libhdgconv.so"))
+_DEFAULT_PATH = os.path.join(HERE, "libhdgconv.so")
+LIB_PATH = os.environ.get("HDGC_LIB", _DEFAULT_PATH)
 
 # exported symbols, in include/hdgconv.h order
 SYMBOLS = (
     "hdgc_create", "hdgc_destroy", "hdgc_get_info", "hdgc_apply_v", "hdgc_apply_w",
     "hdgc_substeps", "hdgc_transfer", "hdgc_mass_inverse", "hdgc_max_speed",
-    "hdgc_apply_v_host", "hdgc_substeps_host", "hdgc_last_error", "hdgc_version",
+    "hdgc_apply_v_host", "hdgc_substeps_host", "hdgc_propagate", "hdgc_richardson",
+    "hdgc_last_error", "hdgc_version",
 )
+
+HDGC_ENOCONV = -5
 
 _dp = C.POINTER(C.c_double)
 
@@ -78,10 +82,15 @@ def load(path: str = LIB_PATH):
         "hdgc_max_speed": ([vp, vp, vp, vp], C.c_int),
         "hdgc_apply_v_host": ([vp, vp, vp, vp, vp, vp], C.c_int),
         "hdgc_substeps_host": ([vp, vp, vp, vp, d, i32, vp], C.c_int),
+        "hdgc_propagate": ([vp, vp, vp, d, d, d, d, i32, i32, vp, vp, vp], C.c_int),
+        "hdgc_richardson": ([vp, vp, vp, vp, d, d, d, i32, vp, C.POINTER(i32), C.POINTER(d), C.POINTER(d), vp],
+                            C.c_int),
         "hdgc_last_error": ([], C.c_char_p),
         "hdgc_version": ([], C.c_char_p),
     }
     for name, (args, res) in sig.items():
+        if path != _DEFAULT_PATH and not hasattr(lib, name):
+            continue      # HDGC_LIB override (development A/B builds): older ABI subsets allowed
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res

@@ -43,8 +43,21 @@ inline int dims_tab(int k) {
 // Output modes of the element kernel.
 enum : int {
   MODE_APPLY = 0,    // r = C^V(u; w)
-  MODE_SUBSTEP = 1,  // w_out = w - dt * (2/detJ) * C^V(u; w)
+  MODE_SUBSTEP = 1,  // w_out = w + c (2/detJ) C^V(u; w)  (forward Euler: c = -dt)
   MODE_APPLY_IT = 2, // r_w = I^T C^V(u; w)
+  MODE_STAGE = 3,    // w_out = a w + b x + c (2/detJ) C^V(u; w), optional residual norms (StageParams)
+};
+
+// Epilogues of the update modes:
+//   MODE_SUBSTEP: out = w + c minv r          (forward Euler / Heun stage 1: c = -dt)
+//   MODE_STAGE:   out = a w + b x + c minv r,
+//                 res = x - w - tau minv r, rn[T * dim + comp] = sum_m res^2 (rn optional)
+// Heun's second stage: a = b = 1/2, c = -dt/2, x = w^n; Richardson
+// (PAPER.md:679-685): a = 1 - ds, b = ds, c = -ds tau, x = g*.
+struct StageParams {
+  const double* __restrict__ x = nullptr;
+  double* __restrict__ rn = nullptr;
+  double a = 1.0, b = 0.0, c = 0.0, tau = 0.0;
 };
 
 // Per-element neighbour code: >= 0: (neighbour element << 2) | neighbour local
@@ -58,7 +71,7 @@ struct ElemParams {
   const double* __restrict__ piola;   // (4, NT) SoA: J/detJ row-major (00, 01, 10, 11)
   const double* __restrict__ minv;    // (NT,) 2/detJ
   double* __restrict__ out;           // (NT, NB)
-  double dt;
+  StageParams st;
   int nt;
 };
 

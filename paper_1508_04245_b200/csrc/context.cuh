@@ -39,6 +39,10 @@ struct hdgc_ctx {
   double* d_hw = nullptr;
   double* d_hr = nullptr;
   double* d_hin = nullptr;
+  double* d_uext = nullptr;     // (NT, nb) extrapolated velocity (propagate, lazily allocated)
+  double* d_rn = nullptr;       // (NT, dim) residual sums of squares (richardson)
+  double* d_sum = nullptr;      // (1,) reduced norm^2
+  double* h_sum = nullptr;      // pinned host copy of d_sum
   void* blas = nullptr;         // cublasHandle_t for the modal GEMM (lazily created)
   int64_t bytes = 0;
   int variant = 0;              // 0: thread-per-element (k <= 2), 1: sum-factorised (k >= 3)
@@ -52,25 +56,25 @@ int hdgc_modal_gemm(hdgc_ctx* c, const double* u, int nb, int nr, size_t off, cu
 namespace hdgc {
 // per-order operations, explicitly instantiated in order_k<K>.cu
 template <int K> int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w,
-                                 const double* inflow, double* out, double dt, cudaStream_t st);
+                                 const double* inflow, double* out, const StageParams& sp, cudaStream_t st);
 template <int K> int launch_transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st);
 template <int K> int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st);
 template <int K> int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st);
 template <int K> int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out,
-                             double dt, cudaStream_t st);
+                             const StageParams& sp, cudaStream_t st);
 template <int K> int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& packed);
 
 // 3D (tetrahedra), order3d_k<K>.cu
 template <int K> int launch3_prep(hdgc_ctx* c, const double* u, cudaStream_t st);
 template <int K> int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out,
-                                  double dt, cudaStream_t st);
+                                  const StageParams& sp, cudaStream_t st);
 template <int K> int launch3_transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st);
 template <int K> int launch3_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st);
 template <int K> int launch3_setup(hdgc_ctx* c, const hdgc_tables_desc* t);
 
 #define HDGC_DECLARE_ORDER3(K)                                                                     \
   extern template int launch3_prep<K>(hdgc_ctx*, const double*, cudaStream_t);                    \
-  extern template int launch3_main<K>(hdgc_ctx*, int, const double*, const double*, double*, double, \
+  extern template int launch3_main<K>(hdgc_ctx*, int, const double*, const double*, double*, const StageParams&, \
                                       cudaStream_t);                                               \
   extern template int launch3_transfer<K>(hdgc_ctx*, int, const double*, double*, cudaStream_t);  \
   extern template int launch3_maxspeed<K>(hdgc_ctx*, const double*, double*, cudaStream_t);      \
@@ -78,11 +82,11 @@ template <int K> int launch3_setup(hdgc_ctx* c, const hdgc_tables_desc* t);
 
 #define HDGC_DECLARE_ORDER(K)                                                                      \
   extern template int launch_elem<K>(hdgc_ctx*, int, const double*, const double*, const double*,  \
-                                     double*, double, cudaStream_t);                               \
+                                     double*, const StageParams&, cudaStream_t);                               \
   extern template int launch_transfer<K>(hdgc_ctx*, int, const double*, double*, cudaStream_t);    \
   extern template int launch_maxspeed<K>(hdgc_ctx*, const double*, double*, cudaStream_t);         \
   extern template int sf_prep<K>(hdgc_ctx*, const double*, cudaStream_t);                          \
-  extern template int sf_main<K>(hdgc_ctx*, int, const double*, const double*, double*, double,    \
+  extern template int sf_main<K>(hdgc_ctx*, int, const double*, const double*, double*, const StageParams&, \
                                  cudaStream_t);                                                    \
   extern template int sf_setup<K>(hdgc_ctx*, const hdgc_tables_desc*, const std::vector<double>&);
 }  // namespace hdgc

@@ -290,7 +290,7 @@ struct SFParams {
   const double* __restrict__ minv;    // (NT,)
   const double* __restrict__ ftab;    // fD[3][NF][NBS] (global copy)
   double* __restrict__ out;           // (NT, NB)
-  double dt;
+  StageParams st;
   int nt;
 };
 
@@ -406,6 +406,25 @@ __device__ __forceinline__ void sf_rows(const double* wc, const double* row, int
   }
 }
 
+// stage epilogue with the extra vector x (SSP-RK2 second stage, Richardson):
+// out = a w + b x + c minv r, optional residual sum of squares (StageParams)
+template <int NBS>
+__device__ __forceinline__ void stage_x(const StageParams& st, double mi, double cm, const double (&r)[NBS],
+                                     const double* part, const double (&wo)[NBS], double* out,
+                                     const double* __restrict__ xg, double* rn) {
+  const double tm = -st.tau * mi;
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < NBS; ++m) {
+    const double rv = r[m] + part[m];
+    const double xv = __ldg(xg + m);
+    out[m] = fma(st.b, xv, fma(cm, rv, st.a * wo[m]));
+    const double res = fma(tm, rv, xv - wo[m]);
+    acc = fma(res, res, acc);
+  }
+  if (rn) *rn = acc;
+}
+
 // Two warps per CTA on one tile of EPB = 16 elements: warp 0 computes the
 // volume term, warp 1 the upwind facet term, concurrently; lane l of either
 // warp owns (element l/2, component l%2).  The facet warp leaves its partial
@@ -460,7 +479,7 @@ conv2d_sf_kernel(SFParams p) {
 
   if (warp == 0) {
     // ===================== volume warp =====================
-    const double sc = MODE == MODE_SUBSTEP && active ? p.dt * __ldg(p.minv + T) : 0.0;
+    const double mi = (MODE == MODE_SUBSTEP || MODE == MODE_STAGE) && active ? __ldg(p.minv + T) : 0.0;
     mbar_wait(bar, 0);
     const double* row = s_prep + (active ? le : 0);        // slot j at row[j * EPB]
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
@@ -472,8 +491,12 @@ conv2d_sf_kernel(SFParams p) {
     if (active) {
       double* wo_s = s_w + le * NB + c * NBS;
       if (MODE == MODE_SUBSTEP) {
+        const double cm = p.st.c * mi;
 #pragma unroll
-        for (int m = 0; m < NBS; ++m) wo_s[m] = fma(-sc, r[m] + part[m], wo[m]);
+        for (int m = 0; m < NBS; ++m) wo_s[m] = fma(cm, r[m] + part[m], wo[m]);
+      } else if (MODE == MODE_STAGE) {
+        stage_x(p.st, mi, p.st.c * mi, r, part, wo, wo_s, p.st.x + (size_t)T * NB + c * NBS,
+                p.st.rn ? p.st.rn + 2 * (size_t)T + c : nullptr);
       } else {
 #pragma unroll
         for (int m = 0; m < NBS; ++m) wo_s[m] = r[m] + part[m];

@@ -188,9 +188,28 @@ conv2d_thread_kernel(ElemParams p) {
 #pragma unroll
     for (int j = 0; j < NB; ++j) og[j] = r[j];
   } else if (MODE == MODE_SUBSTEP) {
-    const double s = p.dt * __ldg(p.minv + T);
+    const double cm = p.st.c * __ldg(p.minv + T);
 #pragma unroll
-    for (int j = 0; j < NB; ++j) og[j] = fma(-s, r[j], w[j]);
+    for (int j = 0; j < NB; ++j) og[j] = fma(cm, r[j], w[j]);
+  } else if (MODE == MODE_STAGE) {
+    const double mi = __ldg(p.minv + T);
+    const double cm = p.st.c * mi;
+    {
+      const double* xg = p.st.x + (size_t)T * NB;
+      const double tm = -p.st.tau * mi;
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const double xv = __ldg(xg + j);
+        og[j] = fma(p.st.b, xv, fma(cm, r[j], p.st.a * w[j]));
+        const double res = fma(tm, r[j], xv - w[j]);
+        if (j < NBS) acc0 = fma(res, res, acc0); else acc1 = fma(res, res, acc1);
+      }
+      if (p.st.rn) {
+        p.st.rn[2 * (size_t)T] = acc0;
+        p.st.rn[2 * (size_t)T + 1] = acc1;
+      }
+    }
   } else {
     // r_w = I^T r: s[d*nbs+m] = sum_c P[c][d] r[c*nbs+m]; r_w[j] = sum_i coef[i][j] s[i]
     const double P00 = __ldg(p.piola + T), P01 = __ldg(p.piola + p.nt + T);

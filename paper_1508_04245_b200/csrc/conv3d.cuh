@@ -178,7 +178,7 @@ struct Conv3Params {
   const int32_t* __restrict__ code;   // (NT, 4)
   const double* __restrict__ minv;    // (NT,) 6/|detJ|
   double* __restrict__ out;
-  double dt;
+  StageParams st;
   int nt;
 };
 
@@ -366,9 +366,25 @@ conv3d_kernel(Conv3Params p) {
   if (!active) return;
   double* og = p.out + (size_t)T * NB + c * NBS;
   if (MODE == MODE_SUBSTEP) {
-    const double sc = p.dt * __ldg(p.minv + T);
+    const double cm = p.st.c * __ldg(p.minv + T);
 #pragma unroll
-    for (int m = 0; m < NBS; ++m) og[m] = fma(-sc, r[m], wo[m]);
+    for (int m = 0; m < NBS; ++m) og[m] = fma(cm, r[m], wo[m]);
+  } else if (MODE == MODE_STAGE) {
+    const double mi = __ldg(p.minv + T);
+    const double cm = p.st.c * mi;
+    {
+      const double* xg = p.st.x + (size_t)T * NB + c * NBS;
+      const double tm = -p.st.tau * mi;
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) {
+        const double xv = __ldg(xg + m);
+        og[m] = fma(p.st.b, xv, fma(cm, r[m], p.st.a * wo[m]));
+        const double res = fma(tm, r[m], xv - wo[m]);
+        acc = fma(res, res, acc);
+      }
+      if (p.st.rn) p.st.rn[3 * (size_t)T + c] = acc;
+    }
   } else {
 #pragma unroll
     for (int m = 0; m < NBS; ++m) og[m] = r[m];

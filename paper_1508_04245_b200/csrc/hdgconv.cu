@@ -60,6 +60,32 @@ int hdgc_modal_gemm(hdgc_ctx* c, const double* u, int nb, int nr, size_t off, cu
   return HDGC_OK;
 }
 
+// out = a x + b y (extrapolated velocity)
+__global__ void axpby_kernel(const double* __restrict__ x, const double* __restrict__ y, double a, double b,
+                             double* __restrict__ out, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = fma(a, x[i], b * y[i]);
+}
+
+// *out = sum v[0..n) in a fixed order (one CTA of 1024 threads: strided partial
+// sums, then a fixed shuffle/smem tree), so residual norms are bitwise
+// reproducible run to run.
+__global__ void __launch_bounds__(1024) sum_kernel(const double* __restrict__ v, size_t n, double* out) {
+  __shared__ double red[32];
+  double a = 0.0;
+  for (size_t i = threadIdx.x; i < n; i += 1024) a += v[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    a = red[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (threadIdx.x == 0) *out = a;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // setup kernels (on-device geometry / adjacency precompute)
 
@@ -178,8 +204,8 @@ HDGC_DECLARE_ORDER(8)
   }
 
 static int elem(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
-                double dt, cudaStream_t st) {
-  HDGC_K_SWITCH(c->k, launch_elem<KK>(c, mode, u, w, inflow, out, dt, st));
+                const StageParams& sp, cudaStream_t st) {
+  HDGC_K_SWITCH(c->k, launch_elem<KK>(c, mode, u, w, inflow, out, sp, st));
 }
 
 static int transfer3(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st);
@@ -193,9 +219,9 @@ static int prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
   HDGC_K_SWITCH(c->k, sf_prep<KK>(c, u, st));
 }
 
-static int sfmain(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, double dt,
+static int sfmain(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, const StageParams& sp,
                   cudaStream_t st) {
-  HDGC_K_SWITCH(c->k, sf_main<KK>(c, mode, w, inflow, out, dt, st));
+  HDGC_K_SWITCH(c->k, sf_main<KK>(c, mode, w, inflow, out, sp, st));
 }
 
 static int setup_variant(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& packed) {
@@ -203,23 +229,34 @@ static int setup_variant(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vect
 }
 
 // one operator application, dispatched on the variant chosen at create
-static int main3(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, double dt,
+static int main3(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, const StageParams& sp,
                  cudaStream_t st);
 static int prep3(hdgc_ctx* c, const double* u, cudaStream_t st);
 
 static int apply_any(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
-                     double dt, bool prep_done, cudaStream_t st) {
+                     const StageParams& sp, bool prep_done, cudaStream_t st) {
   if (c->variant == 2) {
     int rc = prep_done ? HDGC_OK : prep3(c, u, st);
     if (rc) return rc;
-    return main3(c, mode, w, inflow, out, dt, st);
+    return main3(c, mode, w, inflow, out, sp, st);
   }
   if (c->variant == 1) {
     int rc = prep_done ? HDGC_OK : prep(c, u, st);
     if (rc) return rc;
-    return sfmain(c, mode, w, inflow, out, dt, st);
+    return sfmain(c, mode, w, inflow, out, sp, st);
   }
-  return elem(c, mode, u, w, inflow, out, dt, st);
+  return elem(c, mode, u, w, inflow, out, sp, st);
+}
+static int apply_any(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
+                     double dt, bool prep_done, cudaStream_t st) {
+  StageParams sp;
+  sp.c = -dt;
+  return apply_any(c, mode, u, w, inflow, out, sp, prep_done, st);
+}
+static int prep_any(hdgc_ctx* c, const double* u, cudaStream_t st) {
+  if (c->variant == 2) return prep3(c, u, st);
+  if (c->variant == 1) return prep(c, u, st);
+  return HDGC_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -242,9 +279,9 @@ HDGC_DECLARE_ORDER3(4)
   }
 
 static int prep3(hdgc_ctx* c, const double* u, cudaStream_t st) { HDGC_K3_SWITCH(c->k, launch3_prep<KK>(c, u, st)); }
-static int main3(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, double dt,
+static int main3(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, const StageParams& sp,
                  cudaStream_t st) {
-  HDGC_K3_SWITCH(c->k, launch3_main<KK>(c, mode, w, inflow, out, dt, st));
+  HDGC_K3_SWITCH(c->k, launch3_main<KK>(c, mode, w, inflow, out, sp, st));
 }
 static int transfer3(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st) {
   HDGC_K3_SWITCH(c->k, launch3_transfer<KK>(c, dir, in, out, st));
@@ -450,6 +487,8 @@ int hdgc_destroy(hdgc_ctx* c) {
   if (!c) return HDGC_OK;
   cudaFree(c->d_tab); cudaFree(c->d_code); cudaFree(c->d_piola); cudaFree(c->d_minv);
   cudaFree(c->d_sign); cudaFree(c->d_scratch); cudaFree(c->d_scratch2); cudaFree(c->d_modal); cudaFree(c->d_prep); cudaFree(c->d_ftab); cudaFree(c->d_hu); cudaFree(c->d_hw); cudaFree(c->d_hr); cudaFree(c->d_hin);
+  cudaFree(c->d_uext); cudaFree(c->d_rn); cudaFree(c->d_sum);
+  if (c->h_sum) cudaFreeHost(c->h_sum);
   if (c->blas) cublasDestroy(static_cast<cublasHandle_t>(c->blas));
   delete c;
   return HDGC_OK;
@@ -477,7 +516,7 @@ int hdgc_apply_w(hdgc_ctx* c, const double* u, const double* inflow, double* r_w
   cudaStream_t st = (cudaStream_t)stream;
   int rc = transfer(c, 0, u, c->d_scratch, st);
   if (rc) return rc;
-  if (c->variant == 0) return elem(c, MODE_APPLY_IT, u, c->d_scratch, inflow, r_w, 0.0, st);
+  if (c->variant == 0) return elem(c, MODE_APPLY_IT, u, c->d_scratch, inflow, r_w, StageParams(), st);
   // sum-factorised: r_V into scratch2, then I^T
   if (!c->d_scratch2 &&
       (rc = hdgc_dev_alloc(c, (void**)&c->d_scratch2, sizeof(double) * (size_t)c->nt * c->nb)))
@@ -505,6 +544,103 @@ int hdgc_substeps(hdgc_ctx* c, const double* u, double* w, const double* inflow,
     double* t = a; a = b; b = t;
   }
   if (a != w) CUDA_TRY(cudaMemcpyAsync(w, a, sizeof(double) * (size_t)c->nt * c->nb, cudaMemcpyDeviceToDevice, st));
+  return HDGC_OK;
+}
+
+int hdgc_propagate(hdgc_ctx* c, const double* u_prev, const double* u_cur, double t_prev, double t_cur,
+                   double t1, double ds, int32_t nsteps, int32_t scheme, const double* inflow, double* w,
+                   void* stream) {
+  if (!c || !u_cur || !w) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (nsteps < 0) return hdgc_set_err(HDGC_EINVAL, "nsteps < 0");
+  if (scheme != 0 && scheme != 1) return hdgc_set_err(HDGC_EINVAL, "scheme must be 0 (Euler) or 1 (SSP-RK2)");
+  if (w == u_cur || w == u_prev || w == inflow) return hdgc_set_err(HDGC_EINVAL, "w aliases an input");
+  if (u_prev && !(t_cur != t_prev)) return hdgc_set_err(HDGC_EINVAL, "extrapolation needs t_cur != t_prev");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t n = (size_t)c->nt * c->nb;
+  int rc;
+  if (u_prev && !c->d_uext && (rc = hdgc_dev_alloc(c, (void**)&c->d_uext, sizeof(double) * n))) return rc;
+  if (scheme == 1 && !c->d_scratch2 && (rc = hdgc_dev_alloc(c, (void**)&c->d_scratch2, sizeof(double) * n)))
+    return rc;
+  // velocity at pseudo time s; the prep (variants 1/2) is redone only when s changes
+  bool have = false;
+  double at = 0.0;
+  auto velocity = [&](double s, const double** uu) -> int {
+    if (!u_prev) {
+      *uu = u_cur;
+      if (!have) { have = true; return prep_any(c, u_cur, st); }
+      return HDGC_OK;
+    }
+    *uu = c->d_uext;
+    if (have && s == at) return HDGC_OK;
+    const double th = (s - t_cur) / (t_cur - t_prev);
+    axpby_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(u_cur, u_prev, 1.0 + th, -th, c->d_uext, n);
+    CUDA_TRY(cudaGetLastError());
+    have = true;
+    at = s;
+    return prep_any(c, c->d_uext, st);
+  };
+  double* bufs[3] = {w, c->d_scratch, c->d_scratch2};
+  const int nbuf = scheme == 1 ? 3 : 2;   // Euler ping-pongs, Heun rotates v, v1, v'
+  int cur = 0;
+  for (int i = 0; i < nsteps; ++i) {
+    const double s0 = t1 + i * ds, s1 = t1 + (i + 1) * ds;
+    const double* uu = nullptr;
+    if ((rc = velocity(s0, &uu))) return rc;
+    double* v = bufs[cur];
+    double* v1 = bufs[(cur + 1) % nbuf];
+    StageParams sp;
+    sp.c = -ds;
+    if ((rc = apply_any(c, MODE_SUBSTEP, uu, v, inflow, v1, sp, true, st))) return rc;
+    if (scheme == 0) { cur = (cur + 1) % nbuf; continue; }
+    if ((rc = velocity(s1, &uu))) return rc;
+    double* v2 = bufs[(cur + 2) % 3];
+    StageParams s2;
+    s2.a = 0.5; s2.b = 0.5; s2.c = -0.5 * ds; s2.x = v;
+    if ((rc = apply_any(c, MODE_STAGE, uu, v1, inflow, v2, s2, true, st))) return rc;
+    cur = (cur + 2) % 3;
+  }
+  if (bufs[cur] != w) CUDA_TRY(cudaMemcpyAsync(w, bufs[cur], sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  return HDGC_OK;
+}
+
+int hdgc_richardson(hdgc_ctx* c, const double* u, const double* g, const double* inflow, double tau, double ds,
+                    double rho, int32_t max_iter, double* v, int32_t* iters, double* res0, double* res_final,
+                    void* stream) {
+  if (!c || !u || !g || !v) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (max_iter < 0) return hdgc_set_err(HDGC_EINVAL, "max_iter < 0");
+  if (v == u || v == g || v == inflow) return hdgc_set_err(HDGC_EINVAL, "v aliases an input");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t n = (size_t)c->nt * c->nb, nr = (size_t)c->nt * c->dim;
+  int rc;
+  if (!c->d_rn && (rc = hdgc_dev_alloc(c, (void**)&c->d_rn, sizeof(double) * nr))) return rc;
+  if (!c->d_sum && (rc = hdgc_dev_alloc(c, (void**)&c->d_sum, sizeof(double)))) return rc;
+  if (!c->h_sum) CUDA_TRY(cudaMallocHost((void**)&c->h_sum, sizeof(double)));
+  if ((rc = prep_any(c, u, st))) return rc;   // convection frozen over the solve
+  double* a = v;
+  double* b = c->d_scratch;
+  StageParams sp;
+  sp.a = 1.0 - ds; sp.b = ds; sp.c = -ds * tau; sp.tau = tau; sp.x = g; sp.rn = c->d_rn;
+  double r0 = 0.0, rn = 0.0;
+  int it = 0;
+  bool conv = false;
+  for (it = 0; it <= max_iter; ++it) {
+    if ((rc = apply_any(c, MODE_STAGE, u, a, inflow, b, sp, true, st))) return rc;
+    sum_kernel<<<1, 1024, 0, st>>>(c->d_rn, nr, c->d_sum);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(c->h_sum, c->d_sum, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    rn = sqrt(*c->h_sum);
+    if (it == 0) r0 = rn;
+    if (rn <= rho * r0) { conv = true; break; }
+    if (it == max_iter) break;
+    double* t = a; a = b; b = t;          // a = v_{it+1}
+  }
+  if (a != v) CUDA_TRY(cudaMemcpyAsync(v, a, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (iters) *iters = it;
+  if (res0) *res0 = r0;
+  if (res_final) *res_final = rn;
+  if (!conv) return hdgc_set_err(HDGC_ENOCONV, "richardson: ||res|| %.3e > rho ||res_0|| after %d iterations", rn, it);
   return HDGC_OK;
 }
 

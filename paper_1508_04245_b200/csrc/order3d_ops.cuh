@@ -58,7 +58,7 @@ int launch3_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
 }
 
 template <int K>
-int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, double dt,
+int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, const StageParams& sp,
                  cudaStream_t st) {
   Conv3Params p;
   p.tab = c->d_tab;
@@ -69,7 +69,7 @@ int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, d
   p.code = c->d_code;
   p.minv = c->d_minv;
   p.out = out;
-  p.dt = dt;
+  p.st = sp;
   p.nt = c->nt;
   const unsigned blocks = grid3_for(c->nt, Dims3<K>::EPB);
   constexpr int smem = Dims3<K>::SMEM;
@@ -78,7 +78,9 @@ int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, d
     kern<<<blocks, Dims3<K>::THREADS, smem, st>>>(p);
     return HDGC_OK;
   };
-  int rc = mode == MODE_SUBSTEP ? launch(conv3d_kernel<K, MODE_SUBSTEP>) : launch(conv3d_kernel<K, MODE_APPLY>);
+  int rc = mode == MODE_SUBSTEP ? launch(conv3d_kernel<K, MODE_SUBSTEP>)
+           : mode == MODE_STAGE ? launch(conv3d_kernel<K, MODE_STAGE>)
+                                : launch(conv3d_kernel<K, MODE_APPLY>);
   if (rc) return rc;
   CUDA_TRY(cudaGetLastError());
   return HDGC_OK;
@@ -107,7 +109,7 @@ int launch3_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st)
 #define HDGC_INSTANTIATE_ORDER3(K)                                                                  \
   namespace hdgc {                                                                                  \
   template int launch3_prep<K>(hdgc_ctx*, const double*, cudaStream_t);                             \
-  template int launch3_main<K>(hdgc_ctx*, int, const double*, const double*, double*, double, cudaStream_t); \
+  template int launch3_main<K>(hdgc_ctx*, int, const double*, const double*, double*, const StageParams&, cudaStream_t); \
   template int launch3_transfer<K>(hdgc_ctx*, int, const double*, double*, cudaStream_t);           \
   template int launch3_maxspeed<K>(hdgc_ctx*, const double*, double*, cudaStream_t);                \
   template int launch3_setup<K>(hdgc_ctx*, const hdgc_tables_desc*);                               \

@@ -86,9 +86,9 @@ static inline unsigned grid_for(long long work, int threads) { return (unsigned)
 
 template <int K>
 int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow,
-                       double* out, double dt, cudaStream_t st) {
+                       double* out, const StageParams& sp, cudaStream_t st) {
  if constexpr (K > 2) {
-  (void)c; (void)mode; (void)u; (void)w; (void)inflow; (void)out; (void)dt; (void)st;
+  (void)c; (void)mode; (void)u; (void)w; (void)inflow; (void)out; (void)sp; (void)st;
   return hdgc_set_err(HDGC_EUNSUP, "thread-per-element variant is built for k <= 2 only");
  } else {
   ElemParams p;
@@ -100,7 +100,7 @@ int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w, const d
   p.piola = c->d_piola;
   p.minv = c->d_minv;
   p.out = out;
-  p.dt = dt;
+  p.st = sp;
   p.nt = c->nt;
   const int threads = 128;
   const int blocks = (c->nt + threads - 1) / threads;
@@ -114,6 +114,7 @@ int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w, const d
   switch (mode) {
     case MODE_APPLY: return launch(conv2d_thread_kernel<K, MODE_APPLY>);
     case MODE_SUBSTEP: return launch(conv2d_thread_kernel<K, MODE_SUBSTEP>);
+    case MODE_STAGE: return launch(conv2d_thread_kernel<K, MODE_STAGE>);
     default: return launch(conv2d_thread_kernel<K, MODE_APPLY_IT>);
   }
  }
@@ -173,7 +174,7 @@ int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
 }
 
 template <int K>
-int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, double dt,
+int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double* out, const StageParams& sp,
                    cudaStream_t st) {
   if constexpr (K >= 3) {
     using F = SF<K>;
@@ -185,7 +186,7 @@ int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double
     p.minv = c->d_minv;
     p.ftab = c->d_ftab;
     p.out = out;
-    p.dt = dt;
+    p.st = sp;
     p.nt = c->nt;
     const int smem = F::SMEM_DOUBLES * (int)sizeof(double);
     const int blocks = (c->nt + F::EPB - 1) / F::EPB;
@@ -196,6 +197,7 @@ int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double
       return HDGC_OK;
     };
     if (mode == MODE_SUBSTEP) return launch(conv2d_sf_kernel<K, MODE_SUBSTEP>);
+    if (mode == MODE_STAGE) return launch(conv2d_sf_kernel<K, MODE_STAGE>);
     return launch(conv2d_sf_kernel<K, MODE_APPLY>);
   } else {
     return hdgc_set_err(HDGC_EUNSUP, "sum-factorised variant needs k >= 3");
@@ -271,10 +273,10 @@ int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& 
 #define HDGC_INSTANTIATE_ORDER(K)                                                                 \
   namespace hdgc {                                                                                \
   template int launch_elem<K>(hdgc_ctx*, int, const double*, const double*, const double*, double*, \
-                              double, cudaStream_t);                                              \
+                              const StageParams&, cudaStream_t);                                              \
   template int launch_transfer<K>(hdgc_ctx*, int, const double*, double*, cudaStream_t);          \
   template int launch_maxspeed<K>(hdgc_ctx*, const double*, double*, cudaStream_t);               \
   template int sf_prep<K>(hdgc_ctx*, const double*, cudaStream_t);                                \
-  template int sf_main<K>(hdgc_ctx*, int, const double*, const double*, double*, double, cudaStream_t); \
+  template int sf_main<K>(hdgc_ctx*, int, const double*, const double*, double*, const StageParams&, cudaStream_t); \
   template int sf_setup<K>(hdgc_ctx*, const hdgc_tables_desc*, const std::vector<double>&);        \
   }

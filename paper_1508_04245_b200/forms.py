@@ -325,6 +325,51 @@ class ConvectionOperator:
                                           C.c_int32(nsteps), self._stream()), "hdgc_substeps_host")
         return out
 
+    def propagate(self, u_cur, w, ds: float, nsteps: int, inflow=None, scheme: str = "euler",
+                  u_prev=None, t_prev: float = 0.0, t_cur: float = 0.0, t1: float = 0.0):
+        """nsteps explicit substeps of dv/ds = -(M^V)^{-1} C^V(u(s)) v from pseudo
+        time t1: scheme "euler" or "ssprk2" (Heun).  u(s) =
+        u_cur if u_prev is None, else the linear extrapolation through
+        (t_prev, u_prev), (t_cur, u_cur).  Torch input is updated in place."""
+        lib = _lib.load()
+        if scheme not in ("euler", "ssprk2"):
+            raise ValueError("scheme must be 'euler' or 'ssprk2'")
+        ut, _ = self._dev(u_cur, self._vec_shape(), "u_cur")
+        pp = None
+        if u_prev is not None:
+            pt, _ = self._dev(u_prev, self._vec_shape(), "u_prev")
+            pp = C.c_void_p(pt.data_ptr())
+        wt, host = self._dev(w, self._vec_shape(), "w")
+        it, ip = self._inflow(inflow)
+        if not host and wt.data_ptr() != w.data_ptr():
+            raise ValueError("w must be contiguous for the in-place propagation")
+        _lib.check(lib.hdgc_propagate(self._h, pp, C.c_void_p(ut.data_ptr()), C.c_double(t_prev),
+                                      C.c_double(t_cur), C.c_double(t1), C.c_double(ds), C.c_int32(nsteps),
+                                      C.c_int32(0 if scheme == "euler" else 1), ip, C.c_void_p(wt.data_ptr()),
+                                      self._stream()), "hdgc_propagate")
+        return wt.cpu().numpy() if host else wt
+
+    def richardson(self, u, g, v0, tau: float, ds: float, rho: float = 1e-3, max_iter: int = 500,
+                   inflow=None):
+        """Richardson / pseudo-time solve of v + tau (M^V)^{-1} C^V v = g
+        (PAPER.md:671-687).  Returns (v, iterations, converged, res0, res)."""
+        lib = _lib.load()
+        ut, _ = self._dev(u, self._vec_shape(), "u_conv")
+        gt, _ = self._dev(g, self._vec_shape(), "g")
+        vt, host = self._dev(v0, self._vec_shape(), "v0")
+        if vt.data_ptr() == getattr(v0, "data_ptr", lambda: None)():
+            vt = vt.clone()
+        it, ip = self._inflow(inflow)
+        iters, r0, r1 = C.c_int32(0), C.c_double(0.0), C.c_double(0.0)
+        rc = lib.hdgc_richardson(self._h, C.c_void_p(ut.data_ptr()), C.c_void_p(gt.data_ptr()), ip,
+                                 C.c_double(tau), C.c_double(ds), C.c_double(rho), C.c_int32(max_iter),
+                                 C.c_void_p(vt.data_ptr()), C.byref(iters), C.byref(r0), C.byref(r1),
+                                 self._stream())
+        if rc not in (0, _lib.HDGC_ENOCONV):
+            _lib.check(rc, "hdgc_richardson")
+        v = vt.cpu().numpy() if host else vt
+        return v, int(iters.value), rc == 0, float(r0.value), float(r1.value)
+
     def mass_inverse(self):
         """(M^V)^{-1} diagonal: 2/detJ per element."""
         torch = _torch()

@@ -1,0 +1,137 @@
+"""GPU parity of the device-resident time integration (hdgc_propagate,
+hdgc_richardson) against the oracle restatement (oracle/timeloop.py) built
+on the fp64 flux-form oracle apply, 2D (thread and sum-factorised variants)
+and 3D."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import convection as O  # noqa: E402
+from oracle import convection3d as O3  # noqa: E402
+from oracle import timeloop as OT  # noqa: E402
+from paper_1508_04245_b200 import fields as F  # noqa: E402
+from paper_1508_04245_b200 import fields3d as F3  # noqa: E402
+from paper_1508_04245_b200 import mesh as M  # noqa: E402
+from paper_1508_04245_b200 import mesh3d as M3  # noqa: E402
+from paper_1508_04245_b200 import timeloop as TL  # noqa: E402
+from paper_1508_04245_b200.forms import ConvectionData, FEField, FESpace, ConvectionOperator  # noqa: E402
+
+TOL = 1e-10
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else a
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def case2d(k, n=8, wind=None):
+    m = M.generate_structured((0, 0, 1, 1), n, n)
+    kw = {} if wind is None else {"wind": wind}
+    sf = F.StreamFunction(4, 7, **kw)
+    sf0 = F.StreamFunction(4, 8, **kw)
+    u = F.interpolate_curl(m, k, sf)
+    u_prev = F.interpolate_curl(m, k, sf0)
+    w = F.transfer_I_host(m, k, F.interpolate_curl(m, k, F.StreamFunction(4, 9)))
+    inflow = F.inflow_values(m, k, sf)
+    apply = lambda uu, v: O.apply_convection_flux_form(m, k, uu, v, inflow, dtype=np.float64)  # noqa: E731
+    dt = 0.5 * TL.cfl_substep(max(F.max_speed_host(m, k, u), F.max_speed_host(m, k, u_prev)), m.h_min(), k)
+    return m, u, u_prev, w, inflow, apply, O.mass_inverse(m), dt
+
+
+@pytest.mark.parametrize("k", [2, 4])
+@pytest.mark.parametrize("scheme", ["euler", "ssprk2"])
+@pytest.mark.parametrize("extrap", [False, True])
+def test_propagate_vs_oracle(k, scheme, extrap):
+    m, u, u_prev, w, inflow, apply, minv, dt = case2d(k, wind=(1.0, 0.3))
+    op = ConvectionOperator(m, k)
+    n = 12
+    kw = dict(u_prev=u_prev, t_prev=-0.01, t_cur=0.0, t1=0.0) if extrap else {}
+    ref = OT.propagate(apply, minv, u, w, dt, n, scheme, **kw)
+    wd = dev(w)
+    op.propagate(dev(u), wd, dt, n, dev(inflow), scheme,
+                 **({k2: (dev(v) if k2 == "u_prev" else v) for k2, v in kw.items()}))
+    assert rel(wd, ref) < TOL
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_propagate_euler_frozen_equals_substeps(k):
+    m, u, _, w, inflow, _, _, dt = case2d(k)
+    op = ConvectionOperator(m, k)
+    a, b = dev(w), dev(w)
+    op.substeps(dev(u), a, dt, 7, dev(inflow))
+    op.propagate(dev(u), b, dt, 7, dev(inflow), "euler")
+    assert torch.equal(a, b)
+
+
+def test_propagate_convection_api_extrapolated():
+    k = 3
+    m, u, u_prev, w, inflow, apply, minv, _ = case2d(k)
+    sp = FESpace(m, "Hdiv", k)
+    v, nsub, ds = TL.propagate_convection(dev(w), 0.0, 2e-3, FEField(sp, dev(u)), ConvectionData(dev(inflow)),
+                                          scheme="ssprk2", u_prev=FEField(sp, dev(u_prev)), t_prev=-1e-3,
+                                          t_cur=0.0)
+    ref = OT.propagate(apply, minv, u, w, ds, nsub, "ssprk2", u_prev, -1e-3, 0.0, 0.0)
+    assert nsub >= 1 and rel(v, ref) < TOL
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_richardson_vs_oracle(k):
+    m, u, _, w, inflow, apply, minv, dt = case2d(k)
+    op = ConvectionOperator(m, k)
+    g = np.random.default_rng(3).standard_normal(w.shape)
+    tau = 3 * dt
+    ds = TL.richardson_ds(tau, F.max_speed_host(m, k, u), m.h_min(), k)
+    ref, it_ref, conv_ref, r0_ref, _ = OT.richardson(apply, minv, u, g, tau, ds, rho=1e-6, max_iter=300)
+    v, it, conv, r0, _ = op.richardson(dev(u), dev(g), dev(np.zeros_like(g)), tau, ds, 1e-6, 300, dev(inflow))
+    assert conv and conv_ref and it == it_ref
+    assert abs(r0 - r0_ref) < 1e-12 * r0_ref
+    assert rel(v, ref) < TOL
+    # deterministic residual reduction: bitwise identical reruns
+    v2, it2, _, r02, _ = op.richardson(dev(u), dev(g), dev(np.zeros_like(g)), tau, ds, 1e-6, 300, dev(inflow))
+    assert it2 == it and r02 == r0 and torch.equal(v, v2)
+
+
+def test_richardson_trivial_and_flagged():
+    k = 4
+    m, u, _, w, inflow, _, _, dt = case2d(k)
+    op = ConvectionOperator(m, k)
+    g = dev(np.random.default_rng(4).standard_normal(w.shape))
+    v, it, conv, _, _ = op.richardson(dev(u), g, torch.zeros_like(g), 0.0, 1.0, 1e-3, 10, dev(inflow))
+    assert conv and it == 1 and torch.equal(v, g)          # tau = 0: v = g in one iteration
+    sp = FESpace(m, "Hdiv", k)
+    v, it, conv = TL.pseudo_time_solve(g, 0.0, FEField(sp, dev(u)), ConvectionData(dev(inflow)))
+    assert conv and it == 1 and torch.equal(v, g)
+    v, it, conv, r0, rn = op.richardson(dev(u), g, torch.zeros_like(g), 10 * dt, 1e-3, 1e-12, 2, dev(inflow))
+    assert not conv and it == 2 and rn > 1e-12 * r0       # max_iter reached: flagged, not raised
+
+
+def test_propagate_and_richardson_3d():
+    k, n = 2, 3
+    m = M3.generate_cube(n)
+    vp = F3.VectorPotential(3, 11)
+    u = F3.interpolate_curl3(m, k, vp)
+    u_prev = F3.interpolate_curl3(m, k, F3.VectorPotential(3, 12))
+    w = F3.transfer_I3_host(m, k, F3.interpolate_curl3(m, k, F3.VectorPotential(3, 13)))
+    inflow = F3.inflow_values3(m, k, vp)
+    minv = O3.mass_inverse3(m)
+    apply = lambda uu, v: O3.apply_convection3_flux_form(m, k, uu, v, inflow, dtype=np.float64)  # noqa: E731
+    umax = max(F3.max_speed3_host(m, k, u), F3.max_speed3_host(m, k, u_prev))
+    dt = 0.5 * TL.cfl_substep(umax, m.h_min(), k)
+    op = ConvectionOperator(m, k)
+    ref = OT.propagate(apply, minv, u, w, dt, 6, "ssprk2", u_prev, -0.01, 0.0, 0.0)
+    wd = dev(w)
+    op.propagate(dev(u), wd, dt, 6, dev(inflow), "ssprk2", dev(u_prev), -0.01, 0.0, 0.0)
+    assert rel(wd, ref) < TOL
+    g = np.random.default_rng(5).standard_normal(w.shape)
+    tau = 2 * dt
+    ds = TL.richardson_ds(tau, umax, m.h_min(), k)
+    ref, it_ref, _, _, _ = OT.richardson(apply, minv, u, g, tau, ds, rho=1e-6, max_iter=200)
+    v, it, conv, _, _ = op.richardson(dev(u), dev(g), dev(np.zeros_like(g)), tau, ds, 1e-6, 200, dev(inflow))
+    assert conv and it == it_ref and rel(v, ref) < TOL

@@ -43,6 +43,10 @@ METRICS = [
     "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "sm__cycles_elapsed.avg.per_second",
+    "sm__cycles_elapsed.avg",
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed",
 ]
 
 
