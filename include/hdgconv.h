@@ -150,6 +150,21 @@ int hdgc_richardson(hdgc_ctx* ctx, const double* u_loc, const double* g, const d
                     double ds, double rho, int32_t max_iter, double* v_inout, int32_t* iters,
                     double* res0, double* res_final, void* stream);
 
+/* Global H(div) space (fespace.FESpace Hdiv(k)): install the
+ * element -> global dof map, host arrays element_dofs (NT, nb) and factors
+ * (NT, nb) (u_loc[T,j] = factors[T,j] u_glob[element_dofs[T,j]]; every global
+ * dof used by one or two (T, j), 0 <= dof < ndof < 2^31).  Copied to the device;
+ * replaces a previous map.  2D contexts only. */
+int hdgc_set_dofmap(hdgc_ctx* ctx, int64_t ndof, const int64_t* element_dofs, const double* factors);
+/* u_loc = gather(u_glob), (NT, nb) from (ndof,) */
+int hdgc_gather(hdgc_ctx* ctx, const double* u_glob, double* u_loc, void* stream);
+/* r_glob[d] = sum over the (T, j) of d of factors[T,j] r_loc[T,j]: the global
+ * I^T assembly, per dof in a fixed order (no atomics, bitwise reproducible) */
+int hdgc_scatter(hdgc_ctx* ctx, const double* r_loc, double* r_glob, void* stream);
+/* C^U u in global numbering: scatter(I^T C^V(I u_loc; I u_loc)), u_loc = gather(u_glob)
+ * (the convection right-hand side of the Stokes solve). */
+int hdgc_apply_u(hdgc_ctx* ctx, const double* u_glob, const double* inflow, double* r_glob, void* stream);
+
 /* Transfer operators: direction 0: out = I in (BDM -> V_h),
  * direction 1: out = I^T in (V_h functionals -> BDM-test layout). */
 int hdgc_transfer(hdgc_ctx* ctx, int32_t direction, const double* in, double* out, void* stream);

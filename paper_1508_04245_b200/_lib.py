@@ -19,6 +19,7 @@ SYMBOLS = (
     "hdgc_create", "hdgc_destroy", "hdgc_get_info", "hdgc_apply_v", "hdgc_apply_w",
     "hdgc_substeps", "hdgc_transfer", "hdgc_mass_inverse", "hdgc_max_speed",
     "hdgc_apply_v_host", "hdgc_substeps_host", "hdgc_propagate", "hdgc_richardson",
+    "hdgc_set_dofmap", "hdgc_gather", "hdgc_scatter", "hdgc_apply_u",
     "hdgc_last_error", "hdgc_version",
 )
 
@@ -85,6 +86,10 @@ def load(path: str = LIB_PATH):
         "hdgc_propagate": ([vp, vp, vp, d, d, d, d, i32, i32, vp, vp, vp], C.c_int),
         "hdgc_richardson": ([vp, vp, vp, vp, d, d, d, i32, vp, C.POINTER(i32), C.POINTER(d), C.POINTER(d), vp],
                             C.c_int),
+        "hdgc_set_dofmap": ([vp, C.c_int64, vp, vp], C.c_int),
+        "hdgc_gather": ([vp, vp, vp, vp], C.c_int),
+        "hdgc_scatter": ([vp, vp, vp, vp], C.c_int),
+        "hdgc_apply_u": ([vp, vp, vp, vp, vp], C.c_int),
         "hdgc_last_error": ([], C.c_char_p),
         "hdgc_version": ([], C.c_char_p),
     }

@@ -43,6 +43,13 @@ struct hdgc_ctx {
   double* d_rn = nullptr;       // (NT, dim) residual sums of squares (richardson)
   double* d_sum = nullptr;      // (1,) reduced norm^2
   double* h_sum = nullptr;      // pinned host copy of d_sum
+  int64_t ndof = 0;             // global H(div) dof map (hdgc_set_dofmap)
+  int32_t* d_dof = nullptr;     // (NT, nb) global dof of each local dof
+  double* d_dfac = nullptr;     // (NT, nb) local = factor * global
+  int32_t* d_inv = nullptr;     // (ndof, 2) flat local index T*nb+j (or -1), ascending
+  double* d_invf = nullptr;     // (ndof, 2) factors of d_inv
+  double* d_gl = nullptr;       // (NT, nb) gathered u_loc (apply_u)
+  double* d_rw = nullptr;       // (NT, nb) r_W (apply_u)
   void* blas = nullptr;         // cublasHandle_t for the modal GEMM (lazily created)
   int64_t bytes = 0;
   int variant = 0;              // 0: thread-per-element (k <= 2), 1: sum-factorised (k >= 3)

@@ -86,6 +86,22 @@ __global__ void __launch_bounds__(1024) sum_kernel(const double* __restrict__ v,
   }
 }
 
+// global H(div) gather / scatter (fespace dof map)
+__global__ void gather_kernel(const int32_t* __restrict__ dof, const double* __restrict__ fac,
+                              const double* __restrict__ g, double* __restrict__ out, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = fac[i] * __ldg(g + dof[i]);
+}
+__global__ void scatter_kernel(const int32_t* __restrict__ inv, const double* __restrict__ invf,
+                               const double* __restrict__ r, double* __restrict__ out, size_t ndof) {
+  const size_t d = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= ndof) return;
+  const int i0 = inv[2 * d], i1 = inv[2 * d + 1];
+  double a = invf[2 * d] * __ldg(r + i0);
+  if (i1 >= 0) a += invf[2 * d + 1] * __ldg(r + i1);
+  out[d] = a;
+}
+
 // ---------------------------------------------------------------------------
 // setup kernels (on-device geometry / adjacency precompute)
 
@@ -488,6 +504,7 @@ int hdgc_destroy(hdgc_ctx* c) {
   cudaFree(c->d_tab); cudaFree(c->d_code); cudaFree(c->d_piola); cudaFree(c->d_minv);
   cudaFree(c->d_sign); cudaFree(c->d_scratch); cudaFree(c->d_scratch2); cudaFree(c->d_modal); cudaFree(c->d_prep); cudaFree(c->d_ftab); cudaFree(c->d_hu); cudaFree(c->d_hw); cudaFree(c->d_hr); cudaFree(c->d_hin);
   cudaFree(c->d_uext); cudaFree(c->d_rn); cudaFree(c->d_sum);
+  cudaFree(c->d_dof); cudaFree(c->d_dfac); cudaFree(c->d_inv); cudaFree(c->d_invf); cudaFree(c->d_gl); cudaFree(c->d_rw);
   if (c->h_sum) cudaFreeHost(c->h_sum);
   if (c->blas) cublasDestroy(static_cast<cublasHandle_t>(c->blas));
   delete c;
@@ -642,6 +659,71 @@ int hdgc_richardson(hdgc_ctx* c, const double* u, const double* g, const double*
   if (res_final) *res_final = rn;
   if (!conv) return hdgc_set_err(HDGC_ENOCONV, "richardson: ||res|| %.3e > rho ||res_0|| after %d iterations", rn, it);
   return HDGC_OK;
+}
+
+int hdgc_set_dofmap(hdgc_ctx* c, int64_t ndof, const int64_t* element_dofs, const double* factors) {
+  if (!c || !element_dofs || !factors) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (c->dim != 2) return hdgc_set_err(HDGC_EUNSUP, "global H(div) dof map: 2D contexts only");
+  const size_t n = (size_t)c->nt * c->nb;
+  if (ndof <= 0 || ndof >= (int64_t)1 << 31 || n >= (size_t)1 << 31)
+    return hdgc_set_err(HDGC_EINVAL, "ndof %lld out of range", (long long)ndof);
+  std::vector<int32_t> dof(n), inv(2 * (size_t)ndof, -1);
+  std::vector<double> invf(2 * (size_t)ndof, 0.0);
+  for (size_t i = 0; i < n; ++i) {
+    const int64_t d = element_dofs[i];
+    if (d < 0 || d >= ndof) return hdgc_set_err(HDGC_EINVAL, "element_dofs[%zu] = %lld out of range", i, (long long)d);
+    dof[i] = (int32_t)d;
+    int32_t* slot = &inv[2 * (size_t)d];
+    const int s = slot[0] < 0 ? 0 : (slot[1] < 0 ? 1 : 2);
+    if (s == 2) return hdgc_set_err(HDGC_EINVAL, "global dof %lld used by more than two local dofs", (long long)d);
+    slot[s] = (int32_t)i;
+    invf[2 * (size_t)d + s] = factors[i];
+  }
+  for (int64_t d = 0; d < ndof; ++d)
+    if (inv[2 * (size_t)d] < 0) return hdgc_set_err(HDGC_EINVAL, "global dof %lld is not used", (long long)d);
+  cudaFree(c->d_dof); cudaFree(c->d_dfac); cudaFree(c->d_inv); cudaFree(c->d_invf);
+  c->d_dof = nullptr; c->d_dfac = nullptr; c->d_inv = nullptr; c->d_invf = nullptr;
+  int rc;
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_dof, sizeof(int32_t) * n))) return rc;
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_dfac, sizeof(double) * n))) return rc;
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_inv, sizeof(int32_t) * 2 * (size_t)ndof))) return rc;
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_invf, sizeof(double) * 2 * (size_t)ndof))) return rc;
+  CUDA_TRY(cudaMemcpy(c->d_dof, dof.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_dfac, factors, sizeof(double) * n, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_inv, inv.data(), sizeof(int32_t) * inv.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_invf, invf.data(), sizeof(double) * invf.size(), cudaMemcpyHostToDevice));
+  c->ndof = ndof;
+  return HDGC_OK;
+}
+
+int hdgc_gather(hdgc_ctx* c, const double* u_glob, double* u_loc, void* stream) {
+  if (!c || !u_glob || !u_loc) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (!c->d_dof) return hdgc_set_err(HDGC_EINVAL, "no dof map installed (hdgc_set_dofmap)");
+  const size_t n = (size_t)c->nt * c->nb;
+  gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(c->d_dof, c->d_dfac, u_glob, u_loc, n);
+  CUDA_TRY(cudaGetLastError());
+  return HDGC_OK;
+}
+
+int hdgc_scatter(hdgc_ctx* c, const double* r_loc, double* r_glob, void* stream) {
+  if (!c || !r_loc || !r_glob) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (!c->d_inv) return hdgc_set_err(HDGC_EINVAL, "no dof map installed (hdgc_set_dofmap)");
+  const size_t nd = (size_t)c->ndof;
+  scatter_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, (cudaStream_t)stream>>>(c->d_inv, c->d_invf, r_loc, r_glob, nd);
+  CUDA_TRY(cudaGetLastError());
+  return HDGC_OK;
+}
+
+int hdgc_apply_u(hdgc_ctx* c, const double* u_glob, const double* inflow, double* r_glob, void* stream) {
+  if (!c || !u_glob || !r_glob) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (r_glob == u_glob) return hdgc_set_err(HDGC_EINVAL, "output aliases an input");
+  const size_t n = (size_t)c->nt * c->nb;
+  int rc;
+  if (!c->d_gl && (rc = hdgc_dev_alloc(c, (void**)&c->d_gl, sizeof(double) * n))) return rc;
+  if (!c->d_rw && (rc = hdgc_dev_alloc(c, (void**)&c->d_rw, sizeof(double) * n))) return rc;
+  if ((rc = hdgc_gather(c, u_glob, c->d_gl, stream))) return rc;
+  if ((rc = hdgc_apply_w(c, c->d_gl, inflow, c->d_rw, stream))) return rc;
+  return hdgc_scatter(c, c->d_rw, r_glob, stream);
 }
 
 int hdgc_transfer(hdgc_ctx* c, int32_t direction, const double* in, double* out, void* stream) {

@@ -27,7 +27,7 @@ from . import _lib
 from . import basis as B
 
 __all__ = ["FESpace", "FEField", "ConvectionData", "ConvectionOperator", "operator_for",
-           "apply_convection", "apply_convection_W", "apply_transfer", "assemble_mass",
+           "apply_convection", "apply_convection_W", "apply_convection_U", "apply_transfer", "assemble_mass",
            "device_tables"]
 
 
@@ -50,8 +50,25 @@ class FESpace:
 
     @property
     def ndof(self) -> int:
-        # element-local storage; VectorDG matches SPEC.md:183 exactly
+        """SPEC.md:179-183: Hdiv(k) #facets (k+1) + #elements (k+1)(k-1) (global,
+        2D); VectorDG(k) #elements (k+1)(k+2) (element-local storage)."""
+        if self.kind == "Hdiv" and hasattr(self.mesh, "facet_flip"):
+            from .fespace import hdiv_ndof
+            return hdiv_ndof(self.mesh.n_facets, self.mesh.n_elements, self.k)
         return self.mesh.n_elements * self.nb
+
+    def dofmap(self):
+        """Global H(div) dof map (fespace.py), cached per space."""
+        from .fespace import build_hdiv_dofmap
+        key = (id(self.mesh), self.k)
+        dm = _DOFMAPS.get(key)
+        if dm is None or dm[0] is not self.mesh:
+            dm = (self.mesh, build_hdiv_dofmap(self.mesh, self.k))
+            _DOFMAPS[key] = dm
+        return dm[1]
+
+
+_DOFMAPS: dict = {}
 
 
 @dataclass
@@ -370,6 +387,59 @@ class ConvectionOperator:
         v = vt.cpu().numpy() if host else vt
         return v, int(iters.value), rc == 0, float(r0.value), float(r1.value)
 
+    # -- global H(div) numbering ---------------------------------------------------
+
+    def set_dofmap(self, dm):
+        """Install a fespace.HdivDofMap on the device (hdgc_set_dofmap)."""
+        lib = _lib.load()
+        d = np.ascontiguousarray(dm.element_dofs, dtype=np.int64)
+        f = np.ascontiguousarray(dm.factors, dtype=np.float64)
+        if d.shape != self._vec_shape() or f.shape != self._vec_shape():
+            raise ValueError("dof map shape does not match the context")
+        _lib.check(lib.hdgc_set_dofmap(self._h, C.c_int64(dm.ndof), d.ctypes.data_as(C.c_void_p), _ptr(f)),
+                   "hdgc_set_dofmap")
+        self._ndof = int(dm.ndof)
+
+    def _need_dofmap(self):
+        if getattr(self, "_ndof", None) is None:
+            from .fespace import build_hdiv_dofmap
+            self.set_dofmap(build_hdiv_dofmap(self.mesh, self.k))
+        return self._ndof
+
+    def gather(self, u_glob):
+        """u_loc (NT, nb) = factors * u_glob[element_dofs]."""
+        torch = _torch()
+        lib = _lib.load()
+        nd = self._need_dofmap()
+        gt, host = self._dev(u_glob, (nd,), "u_glob")
+        out = torch.empty(self._vec_shape(), dtype=torch.float64, device="cuda")
+        _lib.check(lib.hdgc_gather(self._h, C.c_void_p(gt.data_ptr()), C.c_void_p(out.data_ptr()), self._stream()),
+                   "hdgc_gather")
+        return out.cpu().numpy() if host else out
+
+    def scatter(self, r_loc):
+        """r_glob (ndof,) = global I^T assembly of element-local r_loc (NT, nb)."""
+        torch = _torch()
+        lib = _lib.load()
+        nd = self._need_dofmap()
+        rt, host = self._dev(r_loc, self._vec_shape(), "r_loc")
+        out = torch.empty(nd, dtype=torch.float64, device="cuda")
+        _lib.check(lib.hdgc_scatter(self._h, C.c_void_p(rt.data_ptr()), C.c_void_p(out.data_ptr()), self._stream()),
+                   "hdgc_scatter")
+        return out.cpu().numpy() if host else out
+
+    def apply_u(self, u_glob, inflow=None):
+        """C^U u in global numbering: scatter(I^T C^V(I u_loc; I u_loc)), u_loc = gather(u_glob)."""
+        torch = _torch()
+        lib = _lib.load()
+        nd = self._need_dofmap()
+        gt, host = self._dev(u_glob, (nd,), "u_glob")
+        it, ip = self._inflow(inflow)
+        out = torch.empty(nd, dtype=torch.float64, device="cuda")
+        _lib.check(lib.hdgc_apply_u(self._h, C.c_void_p(gt.data_ptr()), ip, C.c_void_p(out.data_ptr()),
+                                    self._stream()), "hdgc_apply_u")
+        return out.cpu().numpy() if host else out
+
     def mass_inverse(self):
         """(M^V)^{-1} diagonal: 2/detJ per element."""
         torch = _torch()
@@ -428,6 +498,15 @@ def apply_convection_W(u_conv: FEField, data: Optional[ConvectionData] = None):
     sp = u_conv.space
     op = operator_for(sp.mesh, sp.k)
     return op.apply_w(u_conv.coeffs, None if data is None else data.inflow)
+
+
+def apply_convection_U(u_glob, space: FESpace, data: Optional[ConvectionData] = None):
+    """C^U u in the global H(div) numbering (fespace dof map): the convection
+    right-hand side of the Stokes solve."""
+    op = operator_for(space.mesh, space.k)
+    if getattr(op, "_ndof", None) is None:
+        op.set_dofmap(space.dofmap())
+    return op.apply_u(u_glob, None if data is None else data.inflow)
 
 
 def apply_transfer(direction: str, vec, space: FESpace):
