@@ -29,7 +29,8 @@ import numpy as np
 
 from .basis import REF_EDGES
 
-__all__ = ["MeshError", "TriMesh", "build_mesh", "generate_structured", "generate_jittered"]
+__all__ = ["MeshError", "TriMesh", "build_mesh", "generate_structured", "generate_jittered", "load_mesh",
+           "save_mesh"]
 
 
 class MeshError(Exception):
@@ -242,3 +243,66 @@ def generate_jittered(n, amplitude=0.2, seed=0, labels=("left", "right", "bottom
     verts = verts.copy()
     verts[interior] += jit[interior]
     return build_mesh(verts, tris, _structured_markers(n, n, labels))
+
+
+# ---------------------------------------------------------------------------
+# text mesh format (mesh2d.load_mesh, MESH:298-334): header "NV NT NBF", then NV
+# "x y" lines, NT "v0 v1 v2" lines, NBF "v0 v1 label" lines; '#' starts a comment.
+
+
+def load_mesh(path) -> TriMesh:
+    """Read the reference's text mesh format; MeshError("<path>:<line>: ...")
+    on malformed input, as the reference loader reports it."""
+    data = []
+    with open(path) as fh:
+        for no, raw in enumerate(fh, 1):
+            body = raw.partition("#")[0].split()
+            if body:
+                data.append((no, body))
+    if not data:
+        raise MeshError(f"{path}: empty mesh file")
+
+    def fields(entry, conv, expect):
+        no, tok = entry
+        if len(tok) != len(conv):
+            raise MeshError(f"{path}:{no}: expected {expect}")
+        try:
+            return [c(t) for c, t in zip(conv, tok)]
+        except ValueError as err:
+            raise MeshError(f"{path}:{no}: {err}") from None
+
+    nv, nt, nbf = fields(data[0], (int, int, int), "NV NT NBF header")
+    if len(data) != 1 + nv + nt + nbf:
+        raise MeshError(f"{path}: expected {1 + nv + nt + nbf} data lines, got {len(data)}")
+    vsec, tsec, bsec = data[1:1 + nv], data[1 + nv:1 + nv + nt], data[1 + nv + nt:]
+    verts = np.array([fields(e, (float, float), "x y") for e in vsec], dtype=float).reshape(nv, 2)
+    tris = np.array([fields(e, (int, int, int), "v0 v1 v2") for e in tsec], dtype=np.int64).reshape(nt, 3)
+    markers = {}
+    for no, tok in bsec:
+        if len(tok) != 3:
+            raise MeshError(f"{path}:{no}: expected 'v0 v1 label'")
+        try:
+            a, b = int(tok[0]), int(tok[1])
+        except ValueError as err:
+            raise MeshError(f"{path}:{no}: {err}") from None
+        markers[(min(a, b), max(a, b))] = tok[2]
+    for (no, _), t in zip(tsec, tris):
+        if t.min() < 0 or t.max() >= nv:
+            raise MeshError(f"{path}:{no}: vertex index out of range")
+    return build_mesh(verts, tris, markers)
+
+
+def save_mesh(mesh: TriMesh, path) -> None:
+    """Write ``mesh`` in the text format read by load_mesh (labelled boundary
+    facets only; vertex coordinates with 17 significant digits, so a save/load
+    round trip reproduces the mesh bit for bit)."""
+    lab = getattr(mesh, "facet_labels", None) or {}
+    with open(path, "w") as fh:
+        fh.write(f"{mesh.vertices.shape[0]} {mesh.n_elements} {len(lab)}\n")
+        for x, y in mesh.vertices:
+            fh.write(f"{x:.17g} {y:.17g}\n")
+        for a, b, c in mesh.triangles:
+            fh.write(f"{a} {b} {c}\n")
+        for f in sorted(lab):
+            a, b = mesh.facet_vertices[f]
+            fh.write(f"{a} {b} {lab[f]}\n")
