@@ -12,7 +12,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 _DEFAULT_PATH = os.path.join(HERE, "libhdgconv.so")
-LIB_PATH = os.environ.get("HDGC_LIB", _DEFAULT_PATH)
+LIB_PATH = os.environ.get("HDGC_LIB") or _DEFAULT_PATH
 
 # exported symbols, in include/hdgconv.h order
 SYMBOLS = (

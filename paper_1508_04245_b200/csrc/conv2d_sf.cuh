@@ -67,21 +67,34 @@ struct SF {
   static constexpr int FACET_ROWS = HDGC_FACET_ROWS;
 #else
   // volume rows taken by the facet warp to balance the two warps (measured per k)
-  static constexpr int FACET_ROWS = K == 5 ? 1 : (K == 7 ? 2 : 0);
+  static constexpr int FACET_ROWS = K == 5 ? 1 : 0;
 #endif
   static constexpr int PREP_TILE = PREP * 16;      // doubles per tile (EPB = 16)
-  // smem (doubles): mbarrier | prep tile [PREP][EPB] | w tile [EPB][NB] |
-  //                 halo [THREADS][NBS] | fD [3][NF][NBS]
+#ifdef HDGC_SF_RING
+  static constexpr bool RING = HDGC_SF_RING;
+#else
+  // high orders: stream the prep tile row by row through a two-slot smem ring
+  // (cp.async) instead of staging it whole, and keep w in smem instead of
+  // registers: the whole-tile prep (60 KB at k = 8) and the register copy of w
+  // cost occupancy and spills there
+  static constexpr bool RING = K >= 7;
+#endif
+  static constexpr int RING_SLOT = 3 * N * 16;     // alpha | beta | gamma of one row, [3][N][16]
+  // smem (doubles): mbarrier | prep tile [PREP][EPB] or ring [2][3][N][EPB] |
+  //                 w tile [EPB][NB] | halo [THREADS][NBS] | fD [3][NF][NBS]
   static constexpr int SM_BAR = 0;
   static constexpr int SM_PREP = 2;
-  static constexpr int SM_W = SM_PREP + PREP_TILE;
+  static constexpr int SM_W = SM_PREP + (RING ? 2 * RING_SLOT : PREP_TILE);
   static constexpr int SM_HALO = SM_W + EPB * NB;
   static constexpr int SM_FD = SM_HALO + 32 * NBS + ((32 * NBS) & 1);
   // smem edge trace maps R[3][NE][NBS], per-edge stride odd (bank spread across lanes)
   static constexpr int RSTR = (NE * NBS) | 1;
   static constexpr int TAB = 3 * NF * NBS;          // constant-bank facet table size (fD)
   static constexpr int TAB_PAD = (3 * RSTR + 1) & ~1; // smem R table, 16-B multiple for the bulk copy
-  static constexpr int SMEM_DOUBLES = SM_FD + TAB_PAD;
+  // ring mode: B / B' row tables interleaved [N][NBS](B, B') in smem (uniform LDS.128
+  // instead of runtime-indexed constant loads, which ptxas hoists into registers)
+  static constexpr int SM_BT = SM_FD + TAB_PAD;
+  static constexpr int SMEM_DOUBLES = SM_BT + (RING ? 2 * N * NBS : 0);
 };
 
 // The constant-bank tables of the order compiled in this translation unit
@@ -345,64 +358,136 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-// Volume rows [b0, b1) of the collapsed rule for one (element, component):
-// per row b, H_i = sum_j w_ij B_ij(b), H'_i (dB/dy), then values/derivatives at
-// the n points via A_i(xi_a), g = alpha d_xi w + beta d_y|xi w + gamma w, and
-// the test back into r.  wc: w_c in smem; row: the element's prep column.
-template <int K>
-__device__ __forceinline__ void sf_rows(const double* wc, const double* row, int b0, int b1,
-                                        double (&r)[SF<K>::NBS]) {
+#ifndef HDGC_A_UNROLL
+#define HDGC_A_UNROLL 2   // ring mode (k >= 7): measured k=8 474 us vs 572 us fully unrolled
+#endif
+// One volume row b of the collapsed rule for one (element, component):
+// H_i = sum_j w_ij B_ij(b), H'_i (dB/dy), then values/derivatives at the n
+// points via A_i(xi_a), g = alpha d_xi w + beta d_y|xi w + gamma w, and the
+// test back into r.  wv: w_c (register array or smem pointer); al/be/ga: the
+// element's alpha/beta/gamma of row b, point a at [a * EPB].
+template <int K, class WS>
+__device__ __forceinline__ void sf_row(const WS& wv, const double* al, const double* be, const double* ga,
+                                       int b, double (&r)[SF<K>::NBS], const double2* sBT = nullptr) {
   using F = SF<K>;
   constexpr int N = F::N, NE = F::NE, NBS = F::NBS, EPB = F::EPB;
   const double* C = sf_tab<K>();
-  double wo[NBS];
+  const double* Bb = C + F::C_B + b * NBS;
+  const double* Bdb = C + F::C_BD + b * NBS;
+  const double2* BT = sBT + b * NBS;        // ring mode: (B, B') of row b in smem
+  double Hw[NE], Hwd[NE];
 #pragma unroll
-  for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
+  for (int i = 0; i <= K; ++i) {
+    double sw = 0.0, swd = 0.0;
+#pragma unroll
+    for (int j = 0; j <= K - i; ++j) {
+      const int m = midx(i, j);
+      const double x = wv[m];
+      if (F::RING) {
+        const double2 t = BT[m];
+        sw = fma(x, t.x, sw);
+        swd = fma(x, t.y, swd);
+      } else {
+        sw = fma(x, Bb[m], sw);
+        swd = fma(x, Bdb[m], swd);
+      }
+    }
+    Hw[i] = sw;
+    Hwd[i] = swd;
+  }
+  double Kc[NE];
+#pragma unroll
+  for (int i = 0; i <= K; ++i) Kc[i] = 0.0;
+  constexpr int AU = F::RING ? HDGC_A_UNROLL : 64;
+#pragma unroll AU
+  for (int a = 0; a < N; ++a) {
+    double wv0 = 0.0, wxi = 0.0, wyy = 0.0;
+#pragma unroll
+    for (int i = 0; i <= K; ++i) {
+      const double Ai = C[F::C_A + a * NE + i];
+      wv0 = fma(Ai, Hw[i], wv0);
+      wxi = fma(C[F::C_AD + a * NE + i], Hw[i], wxi);
+      wyy = fma(Ai, Hwd[i], wyy);
+    }
+    const double g = fma(al[a * EPB], wxi, fma(be[a * EPB], wyy, ga[a * EPB] * wv0));
+#pragma unroll
+    for (int i = 0; i <= K; ++i) Kc[i] = fma(g, C[F::C_A + a * NE + i], Kc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i <= K; ++i) {
+#pragma unroll
+    for (int j = 0; j <= K - i; ++j) {
+      const int m = midx(i, j);
+      r[m] = fma(Kc[i], F::RING ? BT[m].x : Bb[m], r[m]);
+    }
+  }
+}
+
+// Volume rows [b0, b1) with w_c cached in registers; row: the element's prep
+// column (slot j at row[j * EPB], smem tile or global).
+template <int K>
+__device__ __forceinline__ void sf_rows(const double* wc, const double* row, int b0, int b1,
+                                        double (&r)[SF<K>::NBS], const double2* sBT) {
+  using F = SF<K>;
+  constexpr int N = F::N, NBS = F::NBS, EPB = F::EPB;
+  if constexpr (F::RING) {
 #pragma unroll 1
-  for (int b = b0; b < b1; ++b) {
-    const double* Bb = C + F::C_B + b * NBS;
-    const double* Bdb = C + F::C_BD + b * NBS;
-    double Hw[NE], Hwd[NE];
+    for (int b = b0; b < b1; ++b)
+      sf_row<K>(wc, row + (F::P_AL + b * N) * EPB, row + (F::P_BE + b * N) * EPB, row + (F::P_GA + b * N) * EPB,
+                b, r, sBT);
+  } else {
+    double wo[NBS];
 #pragma unroll
-    for (int i = 0; i <= K; ++i) {
-      double sw = 0.0, swd = 0.0;
+    for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
+#pragma unroll 1
+    for (int b = b0; b < b1; ++b)
+      sf_row<K>(wo, row + (F::P_AL + b * N) * EPB, row + (F::P_BE + b * N) * EPB, row + (F::P_GA + b * N) * EPB,
+                b, r, sBT);
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory");
+}
+
+// Volume rows [0, nrows) for the whole warp, prep streamed row by row from
+// the global tile (gtile, slot-major [PREP][16]) through the two-slot smem
+// ring with cp.async (16-B pieces, all lanes), one row ahead; w_c read from
+// smem (wc).  Lane (le, c): its element's column is le.
+template <int K>
+__device__ __forceinline__ void sf_rows_ring(const double* wc, const double* __restrict__ gtile, double* ring,
+                                             int le, int lane, int nrows, double (&r)[SF<K>::NBS],
+                                             const double2* sBT) {
+  using F = SF<K>;
+  constexpr int N = F::N, EPB = F::EPB;
+  constexpr int PIECES = N * EPB / 2;          // 16-B pieces per alpha/beta/gamma row block
+  auto issue = [&](int b) {
+    double* dst = ring + (b & 1) * F::RING_SLOT;
 #pragma unroll
-      for (int j = 0; j <= K - i; ++j) {
-        const int m = midx(i, j);
-        sw = fma(wo[m], Bb[m], sw);
-        swd = fma(wo[m], Bdb[m], swd);
-      }
-      Hw[i] = sw;
-      Hwd[i] = swd;
+    for (int t = lane; t < 3 * PIECES; t += 32) {
+      const int blk = t / PIECES, off = 2 * (t - blk * PIECES);
+      const int slot = (blk == 0 ? F::P_AL : (blk == 1 ? F::P_BE : F::P_GA)) + b * N;
+      cp_async16(dst + blk * N * EPB + off, gtile + slot * EPB + off);
     }
-    const double* al = row + (F::P_AL + b * N) * EPB;
-    const double* be = row + (F::P_BE + b * N) * EPB;
-    const double* ga = row + (F::P_GA + b * N) * EPB;
-    double Kc[NE];
-#pragma unroll
-    for (int i = 0; i <= K; ++i) Kc[i] = 0.0;
-#pragma unroll
-    for (int a = 0; a < N; ++a) {
-      double wv = 0.0, wxi = 0.0, wyy = 0.0;
-#pragma unroll
-      for (int i = 0; i <= K; ++i) {
-        const double Ai = C[F::C_A + a * NE + i];
-        wv = fma(Ai, Hw[i], wv);
-        wxi = fma(C[F::C_AD + a * NE + i], Hw[i], wxi);
-        wyy = fma(Ai, Hwd[i], wyy);
-      }
-      const double g = fma(al[a * EPB], wxi, fma(be[a * EPB], wyy, ga[a * EPB] * wv));
-#pragma unroll
-      for (int i = 0; i <= K; ++i) Kc[i] = fma(g, C[F::C_A + a * NE + i], Kc[i]);
-    }
-#pragma unroll
-    for (int i = 0; i <= K; ++i) {
-#pragma unroll
-      for (int j = 0; j <= K - i; ++j) {
-        const int m = midx(i, j);
-        r[m] = fma(Kc[i], Bb[m], r[m]);
-      }
-    }
+    cp_async_commit();
+  };
+  issue(0);
+#pragma unroll 1
+  for (int b = 0; b < nrows; ++b) {
+    if (b + 1 < nrows) issue(b + 1);
+    else cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const double* sl = ring + (b & 1) * F::RING_SLOT + le;
+    sf_row<K>(wc, sl, sl + N * EPB, sl + 2 * N * EPB, b, r, sBT);
+    __syncwarp();                                  // slot b & 1 is refilled at b + 1
   }
 }
 
@@ -434,7 +519,7 @@ __device__ __forceinline__ void stage_x(const StageParams& st, double mi, double
 #ifdef HDGC_SF_MINB
 #define HDGC_SF_MINB_OF(K) HDGC_SF_MINB
 #else
-#define HDGC_SF_MINB_OF(K) (K <= 4 ? 6 : (K <= 6 ? 4 : 2))   // register caps 170 / 256 / 255
+#define HDGC_SF_MINB_OF(K) (K <= 4 ? 6 : (K <= 6 ? 4 : 2))   // register caps 170 / 256 / 255 (k >= 7: 4 CTAs/SM by smem + regs)
 #endif
 template <int K, int MODE>
 __global__ void __launch_bounds__(SF<K>::THREADS, HDGC_SF_MINB_OF(K))
@@ -451,17 +536,20 @@ conv2d_sf_kernel(SFParams p) {
 
   const int T0 = blockIdx.x * EPB;
   const int nel = min(EPB, p.nt - T0);
+  double2* s_BT = reinterpret_cast<double2*>(sm + F::SM_BT);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
+  if (F::RING)
+    for (int t = threadIdx.x; t < N * NBS; t += F::THREADS) s_BT[t] = make_double2(C[F::C_B + t], C[F::C_BD + t]);
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t bp = (uint32_t)(F::PREP_TILE * sizeof(double));
+    const uint32_t bp = F::RING ? 0u : (uint32_t)(F::PREP_TILE * sizeof(double));
     const uint32_t bw = (uint32_t)(nel * NB * sizeof(double));
     const uint32_t bt = (uint32_t)(F::TAB_PAD * sizeof(double));
     mbar_arrive_expect_tx(bar, bp + bw + bt);
-    bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
+    if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
     bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
     bulk_g2s(s_fD, p.ftab, bt, bar);
   }
@@ -473,6 +561,9 @@ conv2d_sf_kernel(SFParams p) {
   const bool active = le < nel;
   const int T = T0 + (active ? le : 0);
   double* part = s_halo + lane * NBS;
+  const double* gtile = p.prep + (size_t)blockIdx.x * F::PREP_TILE;
+  // the element's prep column (slot j at row[j * EPB]): smem tile, or (ring) the global tile
+  const double* row = (F::RING ? gtile : s_prep) + (active ? le : 0);
   double r[NBS];
 #pragma unroll
   for (int m = 0; m < NBS; ++m) r[m] = 0.0;
@@ -481,15 +572,15 @@ conv2d_sf_kernel(SFParams p) {
     // ===================== volume warp =====================
     const double mi = (MODE == MODE_SUBSTEP || MODE == MODE_STAGE) && active ? __ldg(p.minv + T) : 0.0;
     mbar_wait(bar, 0);
-    const double* row = s_prep + (active ? le : 0);        // slot j at row[j * EPB]
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
-    double wo[NBS];
-#pragma unroll
-    for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
-    sf_rows<K>(wc, row, 0, N - F::FACET_ROWS, r);
+    if (F::RING) sf_rows_ring<K>(wc, gtile, s_prep, active ? le : 0, lane, N - F::FACET_ROWS, r, s_BT);
+    else sf_rows<K>(wc, row, 0, N - F::FACET_ROWS, r, s_BT);
     asm volatile("bar.sync 1, 64;\n" ::: "memory");   // (A) facet partial r ready, in-tile w reads done
     if (active) {
       double* wo_s = s_w + le * NB + c * NBS;
+      double wo[NBS];
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) wo[m] = wo_s[m];
       if (MODE == MODE_SUBSTEP) {
         const double cm = p.st.c * mi;
 #pragma unroll
@@ -514,7 +605,6 @@ conv2d_sf_kernel(SFParams p) {
 #pragma unroll
     for (int ed = 0; ed < 3; ++ed) codes[ed] = active ? __ldg(p.code + (size_t)T * 3 + ed) : -1;
     mbar_wait(bar, 0);
-    const double* row = s_prep + (active ? le : 0);        // slot j at row[j * EPB]
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
     double* halo = part;
     int halo_edge = -1;
@@ -535,9 +625,6 @@ conv2d_sf_kernel(SFParams p) {
         for (int m = 0; m < NBS; ++m) cp_async8(halo + m, g + m);
       }
     }
-    double wo[NBS];
-#pragma unroll
-    for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
     if (halo_edge >= 0) cp_async_wait_all();
     __shared__ double zero_row[NBS];
     for (int m = lane; m < NBS; m += 32) zero_row[m] = 0.0;
@@ -620,7 +707,7 @@ conv2d_sf_kernel(SFParams p) {
       }
     }
     // balance: the facet warp also takes the last FACET_ROWS volume rows
-    if (F::FACET_ROWS > 0) sf_rows<K>(wc, row, N - F::FACET_ROWS, N, r);
+    if (F::FACET_ROWS > 0) sf_rows<K>(wc, row, N - F::FACET_ROWS, N, r, s_BT);
     __syncwarp();          // halo reads of all lanes done before the partials overwrite it
 #pragma unroll
     for (int m = 0; m < NBS; ++m) part[m] = r[m];

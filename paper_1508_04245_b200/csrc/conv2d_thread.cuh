@@ -1,6 +1,5 @@
-// Variant "thread": one thread per element, fused volume + upwind facets,
-// tables broadcast from shared memory.  Generic in K (1..8); the fallback for
-// orders without a tuned variant.
+// Variant "thread" (k <= 2): one thread per element, fused volume + upwind
+// facets, tables as constant-bank operands (fully unrolled point loops).
 //
 // Operator, geometry-free reference form
 // on affine elements, evaluated in the equivalent
@@ -21,34 +20,43 @@
 
 namespace hdgc {
 
-template <int K>
-__host__ __device__ constexpr bool thread_tab_in_smem() { return Dims<K>::TAB * 8 <= 200 * 1024; }
+#ifndef HDGC_ORDER
+#error "define HDGC_ORDER before including conv2d_thread.cuh"
+#endif
+#if HDGC_ORDER <= 2
+// the packed reference tables of this translation unit's order (Dims<K> layout)
+// in the constant bank: with every loop over points and edges unrolled, each
+// table entry is an immediate uniform operand of its DFMA (no LDS per FMA)
+__constant__ double c_th[Dims<HDGC_ORDER>::TAB];
+#else
+__constant__ double c_th[1];
+#endif
 
 template <int K>
-__host__ __device__ constexpr int thread_smem_bytes() { return thread_tab_in_smem<K>() ? Dims<K>::TAB * 8 : 0; }
+__host__ __device__ constexpr int thread_smem_bytes() { return 3 * Dims<K>::NF * Dims<K>::NBS * 8; }
+
+constexpr int THREAD_BLOCK = 64;   // small blocks: 2048 CTAs at 131k elements fill the SMs in ~2 full waves
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(THREAD_BLOCK)
 conv2d_thread_kernel(ElemParams p) {
+  static_assert(K == HDGC_ORDER && K <= 2, "thread variant: k <= 2, tables per translation unit");
   using D = Dims<K>;
   constexpr int NB = D::NB, NBS = D::NBS, NBS1 = D::NBS1, NE = D::NE, NF = D::NF, NQV = D::NQV;
-  // tables staged in shared memory when they fit (k <= 7), else read through L1
-  constexpr bool SMEM = thread_tab_in_smem<K>();
-  extern __shared__ __align__(16) double s_tab[];
-  if (SMEM) {
-    for (int i = threadIdx.x; i < D::TAB; i += blockDim.x) s_tab[i] = p.tab[i];
-    __syncthreads();
-  }
-  const double* base = SMEM ? s_tab : p.tab;
-  const double* coef = base + D::OFF_COEF;
-  const double* divm = base + D::OFF_DIVM;
-  const double* vw = base + D::OFF_VW;
-  const double* vD = base + D::OFF_VD;
-  const double* vG = base + D::OFF_VG;
-  const double* fw = base + D::OFF_FW;
-  const double* fL = base + D::OFF_FL;
-  const double* fD = base + D::OFF_FD;
-  const double* flen = base + D::OFF_FLEN;
+  const double* coef = c_th + D::OFF_COEF;
+  const double* divm = c_th + D::OFF_DIVM;
+  const double* vw = c_th + D::OFF_VW;
+  const double* vD = c_th + D::OFF_VD;
+  const double* vG = c_th + D::OFF_VG;
+  const double* fw = c_th + D::OFF_FW;
+  const double* fL = c_th + D::OFF_FL;
+  const double* fD = c_th + D::OFF_FD;
+  const double* flen = c_th + D::OFF_FLEN;
+  // neighbour-side facet traces are indexed by the neighbour's local edge (per
+  // lane): from a shared-memory copy instead of divergent constant loads
+  extern __shared__ __align__(16) double s_fD[];
+  for (int i = threadIdx.x; i < 3 * NF * NBS; i += blockDim.x) s_fD[i] = p.tab[D::OFF_FD + i];
+  __syncthreads();
 
   const int T = blockIdx.x * blockDim.x + threadIdx.x;
   if (T >= p.nt) return;
@@ -58,9 +66,13 @@ conv2d_thread_kernel(ElemParams p) {
   double dv[NBS1];
   {
     double u[NB];
-    const double* ug = p.u + (size_t)T * NB;
+    const double2* ug = reinterpret_cast<const double2*>(p.u + (size_t)T * NB);
 #pragma unroll
-    for (int j = 0; j < NB; ++j) u[j] = __ldg(ug + j);
+    for (int j = 0; j < NB / 2; ++j) {
+      const double2 t = __ldg(ug + j);
+      u[2 * j] = t.x;
+      u[2 * j + 1] = t.y;
+    }
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       double a = 0.0;
@@ -78,16 +90,20 @@ conv2d_thread_kernel(ElemParams p) {
   }
   double w[NB];
   {
-    const double* wg = p.w + (size_t)T * NB;
+    const double2* wg = reinterpret_cast<const double2*>(p.w + (size_t)T * NB);
 #pragma unroll
-    for (int j = 0; j < NB; ++j) w[j] = __ldg(wg + j);
+    for (int j = 0; j < NB / 2; ++j) {
+      const double2 t = __ldg(wg + j);
+      w[2 * j] = t.x;
+      w[2 * j + 1] = t.y;
+    }
   }
   double r[NB];
 #pragma unroll
   for (int j = 0; j < NB; ++j) r[j] = 0.0;
 
   // ---- volume: f_c = u.grad w_c + w_c div u, tested against D_m
-#pragma unroll 1
+#pragma unroll
   for (int q = 0; q < NQV; ++q) {
     const double* Dq = vD + q * NBS;
     const double* Gq = vG + q * NBS * 2;
@@ -117,7 +133,7 @@ conv2d_thread_kernel(ElemParams p) {
   }
 
   // ---- facets: upwind jump on inflow points only (element-owned, no atomics)
-#pragma unroll 1
+#pragma unroll
   for (int e = 0; e < 3; ++e) {
     double ue[NE];
 #pragma unroll
@@ -161,7 +177,7 @@ conv2d_thread_kernel(ElemParams p) {
       }
       double x0, x1;
       if (code >= 0) {
-        const double* Dn = fD + (e2 * NF + (NF - 1 - q)) * NBS;
+        const double* Dn = s_fD + (e2 * NF + (NF - 1 - q)) * NBS;
         x0 = 0.0; x1 = 0.0;
 #pragma unroll
         for (int m = 0; m < NBS; ++m) {

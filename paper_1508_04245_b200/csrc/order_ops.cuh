@@ -102,7 +102,7 @@ int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w, const d
   p.out = out;
   p.st = sp;
   p.nt = c->nt;
-  const int threads = 128;
+  const int threads = THREAD_BLOCK;
   const int blocks = (c->nt + threads - 1) / threads;
   const int smem = thread_smem_bytes<K>();
   auto launch = [&](auto kern) -> int {
@@ -263,7 +263,9 @@ int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& 
     c->variant = 1;
     return HDGC_OK;
   } else {
-    (void)c; (void)t; (void)packed;
+    // thread-per-element variant: the packed tables into this order's constant bank
+    (void)t;
+    CUDA_TRY(cudaMemcpyToSymbol(c_th, packed.data(), sizeof(double) * Dims<K>::TAB));
     return HDGC_OK;
   }
 }
