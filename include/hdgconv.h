@@ -169,8 +169,25 @@ int hdgc_apply_u(hdgc_ctx* ctx, const double* u_glob, const double* inflow, doub
  * direction 1: out = I^T in (V_h functionals -> BDM-test layout). */
 int hdgc_transfer(hdgc_ctx* ctx, int32_t direction, const double* in, double* out, void* stream);
 
-/* (M^V)^{-1} diagonal scale per element, out (NT,) = 2/detJ. */
+/* (M^V)^{-1} diagonal scale per element, out (NT,) = 2/detJ;
+ * on a curved element (hdgc_set_curved) the entry is -(slot + 1), its
+ * (M^V)^{-1} being the full block minv_blocks[slot]. */
 int hdgc_mass_inverse(hdgc_ctx* ctx, double* out, void* stream);
+
+/* Curved elements (mesh2d.curve_boundary, MESH:555-615):
+ * install, once per 2D context, the n elements carrying an isoparametric map
+ * (ascending ids, HOST arrays, copied):
+ *   minv_blocks (n, nbs, nbs)  inverse V_h mass blocks, M_T = int D_m D_n detJ
+ *                              (same block for both components);
+ *   itrans      (n, nb, nb)    I_T, the element L2 projection BDM -> V_h
+ *                              (rows c*nbs+m, columns BDM members); I^T = I_T^T;
+ *   piola       (n, nqv, 4)    J/detJ at the volume points (max_speed).
+ * The convection apply itself is unchanged (geometry-free reference form, exact
+ * with Piola velocities and pulled-back test functions); substeps, propagate
+ * and richardson apply the block inverse, transfer / apply_w / apply_u use I_T,
+ * max_speed the per-point Piola factor.  2D only (HDGC_EUNSUP in 3D). */
+int hdgc_set_curved(hdgc_ctx* ctx, int32_t n, const int32_t* elems, const double* minv_blocks,
+                    const double* itrans, const double* piola);
 
 /* max over elements x volume points of |J u_hat / detJ| into *out_dev (device
  * double), for the substep size dt = 0.1 h / (k^2 max|u|) (BASELINE cfg2). */

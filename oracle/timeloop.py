@@ -17,8 +17,9 @@ convection time integration built on the apply (SPEC.md ``timeloop``):
   is restated here.
 
 Both are generic over ``apply(u, v) -> r`` (C^V(u; v) in V_h layout) and the
-per-element mass inverse ``minv`` (NT,), so the same restatement checks the
-2D and 3D device paths.  Only tests/ may import this module.
+mass inverse ``minv``: a per-element diagonal (NT,), or a callable applying
+the block-diagonal (M^V)^{-1} of a curved mesh, so the same
+restatement checks the 2D, curved and 3D device paths.  Only tests/ may import this module.
 """
 from __future__ import annotations
 
@@ -33,30 +34,37 @@ def velocity_at(s, u_cur, u_prev=None, t_prev=0.0, t_cur=0.0):
     return (1.0 + th) * u_cur - th * u_prev
 
 
+def _mass_inv(minv):
+    if callable(minv):
+        return minv
+    mi = np.asarray(minv, dtype=float)[:, None]
+    return lambda r: mi * r
+
+
 def propagate(apply, minv, u_cur, w0, ds, nsteps, scheme="euler", u_prev=None, t_prev=0.0, t_cur=0.0,
               t1=0.0):
     """nsteps substeps from pseudo time t1; scheme "euler" or "ssprk2" (Heun:
     v1 = v - ds M^-1 C(s) v, v' = (v + v1 - ds M^-1 C(s+ds) v1) / 2)."""
-    mi = np.asarray(minv, dtype=float)[:, None]
+    mi = _mass_inv(minv)
     v = np.array(w0, dtype=float, copy=True)
     for i in range(nsteps):
         s0, s1 = t1 + i * ds, t1 + (i + 1) * ds
-        v1 = v - ds * mi * apply(velocity_at(s0, u_cur, u_prev, t_prev, t_cur), v)
+        v1 = v - ds * mi(apply(velocity_at(s0, u_cur, u_prev, t_prev, t_cur), v))
         if scheme == "euler":
             v = v1
             continue
-        v2 = v1 - ds * mi * apply(velocity_at(s1, u_cur, u_prev, t_prev, t_cur), v1)
+        v2 = v1 - ds * mi(apply(velocity_at(s1, u_cur, u_prev, t_prev, t_cur), v1))
         v = 0.5 * v + 0.5 * v2
     return v
 
 
 def richardson(apply, minv, u, g, tau, ds, rho=1e-3, max_iter=500, v0=None):
     """Returns (v, iterations, converged, res0, res)."""
-    mi = np.asarray(minv, dtype=float)[:, None]
+    mi = _mass_inv(minv)
     v = np.zeros_like(g, dtype=float) if v0 is None else np.array(v0, dtype=float, copy=True)
     r0 = None
     for it in range(max_iter + 1):
-        res = g - v - tau * mi * apply(u, v)
+        res = g - v - tau * mi(apply(u, v))
         rn = float(np.sqrt(np.sum(res * res)))
         if r0 is None:
             r0 = rn

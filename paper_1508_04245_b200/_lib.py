@@ -19,7 +19,7 @@ SYMBOLS = (
     "hdgc_create", "hdgc_destroy", "hdgc_get_info", "hdgc_apply_v", "hdgc_apply_w",
     "hdgc_substeps", "hdgc_transfer", "hdgc_mass_inverse", "hdgc_max_speed",
     "hdgc_apply_v_host", "hdgc_substeps_host", "hdgc_propagate", "hdgc_richardson",
-    "hdgc_set_dofmap", "hdgc_gather", "hdgc_scatter", "hdgc_apply_u",
+    "hdgc_set_dofmap", "hdgc_gather", "hdgc_scatter", "hdgc_apply_u", "hdgc_set_curved",
     "hdgc_last_error", "hdgc_version",
 )
 
@@ -90,6 +90,7 @@ def load(path: str = LIB_PATH):
         "hdgc_gather": ([vp, vp, vp, vp], C.c_int),
         "hdgc_scatter": ([vp, vp, vp, vp], C.c_int),
         "hdgc_apply_u": ([vp, vp, vp, vp, vp], C.c_int),
+        "hdgc_set_curved": ([vp, i32, vp, vp, vp, vp], C.c_int),
         "hdgc_last_error": ([], C.c_char_p),
         "hdgc_version": ([], C.c_char_p),
     }

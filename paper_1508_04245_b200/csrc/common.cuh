@@ -54,9 +54,14 @@ enum : int {
 //                 res = x - w - tau minv r, rn[T * dim + comp] = sum_m res^2 (rn optional)
 // Heun's second stage: a = b = 1/2, c = -dt/2, x = w^n; Richardson
 // (PAPER.md:679-685): a = 1 - ds, b = ds, c = -ds tau, x = g*.
+// Curved elements (hdgc_set_curved): their mass is a full block, flagged by a
+// negative minv[T] = -(slot + 1).  The update kernels then store the raw
+// residual row into cres[slot] and curved_fixup_kernel applies the block
+// inverse afterwards (the kernels' own output for those rows is overwritten).
 struct StageParams {
   const double* __restrict__ x = nullptr;
   double* __restrict__ rn = nullptr;
+  double* __restrict__ cres = nullptr;   // (n_curved, NB) raw residual rows of curved elements
   double a = 1.0, b = 0.0, c = 0.0, tau = 0.0;
 };
 

@@ -51,6 +51,13 @@ struct hdgc_ctx {
   double* d_gl = nullptr;       // (NT, nb) gathered u_loc (apply_u)
   double* d_rw = nullptr;       // (NT, nb) r_W (apply_u)
   void* blas = nullptr;         // cublasHandle_t for the modal GEMM (lazily created)
+  // curved elements (hdgc_set_curved): d_minv[T] = -(slot + 1) marks them
+  int n_curved = 0;
+  int32_t* d_celems = nullptr;  // (n_curved,) element ids, ascending
+  double* d_cminv = nullptr;    // (n_curved, nbs, nbs) inverse mass blocks
+  double* d_citrans = nullptr;  // (n_curved, nb, nb) I_T (L2 projection), I^T = I_T^T
+  double* d_cpiola = nullptr;   // (n_curved, nqv, 4) J/detJ at the volume points
+  double* d_cres = nullptr;     // (n_curved, nb) raw residual rows (update kernels -> fix-up)
   int64_t bytes = 0;
   int variant = 0;              // 0: thread-per-element (k <= 2), 1: sum-factorised (k >= 3)
 };

@@ -581,6 +581,12 @@ conv2d_sf_kernel(SFParams p) {
       double wo[NBS];
 #pragma unroll
       for (int m = 0; m < NBS; ++m) wo[m] = wo_s[m];
+      if ((MODE == MODE_SUBSTEP || MODE == MODE_STAGE) && mi < 0.0 && p.st.cres) {
+        // curved element: hand the raw residual to curved_fixup_kernel
+        double* cr = p.st.cres + (size_t)((int)(-mi) - 1) * NB + c * NBS;
+#pragma unroll
+        for (int m = 0; m < NBS; ++m) cr[m] = r[m] + part[m];
+      }
       if (MODE == MODE_SUBSTEP) {
         const double cm = p.st.c * mi;
 #pragma unroll

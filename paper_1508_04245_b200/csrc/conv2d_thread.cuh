@@ -200,6 +200,15 @@ conv2d_thread_kernel(ElemParams p) {
 
   // ---- epilogue
   double* og = p.out + (size_t)T * NB;
+  if ((MODE == MODE_SUBSTEP || MODE == MODE_STAGE) && p.st.cres) {
+    const double mflag = __ldg(p.minv + T);
+    if (mflag < 0.0) {
+      // curved element: hand the raw residual to curved_fixup_kernel
+      double* cr = p.st.cres + (size_t)((int)(-mflag) - 1) * NB;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) cr[j] = r[j];
+    }
+  }
   if (MODE == MODE_APPLY) {
 #pragma unroll
     for (int j = 0; j < NB; ++j) og[j] = r[j];

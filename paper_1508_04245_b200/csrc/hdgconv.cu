@@ -219,6 +219,95 @@ HDGC_DECLARE_ORDER(8)
     default: return hdgc_set_err(HDGC_EUNSUP, "order k=%d not supported (1..8)", k); \
   }
 
+// ---------------------------------------------------------------------------
+// Curved elements (hdgc_set_curved).  A few
+// elements along a curved boundary: small generic kernels, one thread per
+// (curved element, component) or (curved element, row).
+
+// minv[T] = -(slot + 1) flags a curved element for the update kernels
+__global__ void mark_curved_kernel(const int32_t* __restrict__ el, int n, double* __restrict__ minv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) minv[el[i]] = -(double)(i + 1);
+}
+
+// update epilogues of the curved rows with the full block inverse:
+//   SUBSTEP: out = w + c M^-1 r;   STAGE: out = a w + b x + c M^-1 r,
+//   rn[T, comp] = sum_m (x - w - tau M^-1 r)^2
+__global__ void curved_fixup_kernel(int mode, const int32_t* __restrict__ el, int n, int nbs,
+                                    const double* __restrict__ minv, const double* __restrict__ cres,
+                                    const double* __restrict__ w, double* __restrict__ out, StageParams sp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * n) return;
+  const int slot = i >> 1, comp = i & 1, nb = 2 * nbs;
+  const size_t T = (size_t)el[slot];
+  const double* Mi = minv + (size_t)slot * nbs * nbs;
+  const double* r = cres + (size_t)slot * nb + comp * nbs;
+  double acc = 0.0;
+  for (int m = 0; m < nbs; ++m) {
+    double s = 0.0;
+    for (int l = 0; l < nbs; ++l) s = fma(Mi[m * nbs + l], r[l], s);
+    const size_t g = T * nb + comp * nbs + m;
+    if (mode == MODE_SUBSTEP) {
+      out[g] = fma(sp.c, s, w[g]);
+    } else {
+      const double xv = sp.x[g];
+      out[g] = fma(sp.b, xv, fma(sp.c, s, sp.a * w[g]));
+      const double res = fma(-sp.tau, s, xv - w[g]);
+      acc = fma(res, res, acc);
+    }
+  }
+  if (mode == MODE_STAGE && sp.rn) sp.rn[2 * T + comp] = acc;
+}
+
+// transfer rows of curved elements: I (dir 0) out = I_T in, I^T (dir 1) out = I_T^T in
+__global__ void curved_transfer_kernel(int dir, const int32_t* __restrict__ el, int n, int nb,
+                                       const double* __restrict__ itrans, const double* __restrict__ in,
+                                       double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * nb) return;
+  const int slot = i / nb, row = i - slot * nb;
+  const size_t T = (size_t)el[slot];
+  const double* It = itrans + (size_t)slot * nb * nb;
+  const double* x = in + T * nb;
+  double a = 0.0;
+  if (dir == 0)
+    for (int j = 0; j < nb; ++j) a = fma(It[row * nb + j], x[j], a);
+  else
+    for (int j = 0; j < nb; ++j) a = fma(It[j * nb + row], x[j], a);
+  out[T * nb + row] = a;
+}
+
+// max |J u_hat / detJ| over the curved elements' volume points (per-point J),
+// from the modal rows (u_hat | div) of launch_maxspeed's DGEMM
+__global__ void curved_maxspeed_kernel(const int32_t* __restrict__ el, int n, int nbs, int mr, int nqv,
+                                       const double* __restrict__ vD, const double* __restrict__ modal,
+                                       const double* __restrict__ cpiola, unsigned long long* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double best = 0.0;
+  if (i < n * nqv) {
+    const int slot = i / nqv, q = i - slot * nqv;
+    const double* mrow = modal + (size_t)el[slot] * mr;
+    double a = 0.0, b = 0.0;
+    for (int m = 0; m < nbs; ++m) {
+      a = fma(mrow[m], vD[q * nbs + m], a);
+      b = fma(mrow[nbs + m], vD[q * nbs + m], b);
+    }
+    const double* P = cpiola + ((size_t)slot * nqv + q) * 4;
+    const double x = fma(P[0], a, P[1] * b), y = fma(P[2], a, P[3] * b);
+    best = sqrt(fma(x, x, y * y));
+  }
+  for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
+}
+
+static int curved_fixup(hdgc_ctx* c, int mode, const double* w, double* out, const StageParams& sp, cudaStream_t st) {
+  const int th = 128;
+  curved_fixup_kernel<<<(2 * c->n_curved + th - 1) / th, th, 0, st>>>(mode, c->d_celems, c->n_curved, c->nbs,
+                                                                    c->d_cminv, c->d_cres, w, out, sp);
+  CUDA_TRY(cudaGetLastError());
+  return HDGC_OK;
+}
+
 static int elem(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
                 const StageParams& sp, cudaStream_t st) {
   HDGC_K_SWITCH(c->k, launch_elem<KK>(c, mode, u, w, inflow, out, sp, st));
@@ -226,9 +315,20 @@ static int elem(hdgc_ctx* c, int mode, const double* u, const double* w, const d
 
 static int transfer3(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st);
 
+static int transfer_affine(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st) {
+  HDGC_K_SWITCH(c->k, launch_transfer<KK>(c, dir, in, out, st));
+}
+
 static int transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st) {
   if (c->dim == 3) return transfer3(c, dir, in, out, st);
-  HDGC_K_SWITCH(c->k, launch_transfer<KK>(c, dir, in, out, st));
+  int rc = transfer_affine(c, dir, in, out, st);
+  if (rc || c->n_curved == 0) return rc;
+  // curved rows: the L2 projection I_T replaces the affine embedding
+  const int th = 128, work = c->n_curved * c->nb;
+  curved_transfer_kernel<<<(work + th - 1) / th, th, 0, st>>>(dir, c->d_celems, c->n_curved, c->nb, c->d_citrans,
+                                                             in, out);
+  CUDA_TRY(cudaGetLastError());
+  return HDGC_OK;
 }
 
 static int prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
@@ -249,8 +349,19 @@ static int main3(hdgc_ctx* c, int mode, const double* w, const double* inflow, d
                  cudaStream_t st);
 static int prep3(hdgc_ctx* c, const double* u, cudaStream_t st);
 
+static int apply_any_(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
+                      const StageParams& sp, bool prep_done, cudaStream_t st);
 static int apply_any(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
-                     const StageParams& sp, bool prep_done, cudaStream_t st) {
+                     const StageParams& sp0, bool prep_done, cudaStream_t st) {
+  if (c->n_curved == 0 || (mode != MODE_SUBSTEP && mode != MODE_STAGE))
+    return apply_any_(c, mode, u, w, inflow, out, sp0, prep_done, st);
+  StageParams sp = sp0;
+  sp.cres = c->d_cres;
+  int rc = apply_any_(c, mode, u, w, inflow, out, sp, prep_done, st);
+  return rc ? rc : curved_fixup(c, mode, w, out, sp, st);
+}
+static int apply_any_(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
+                      const StageParams& sp, bool prep_done, cudaStream_t st) {
   if (c->variant == 2) {
     int rc = prep_done ? HDGC_OK : prep3(c, u, st);
     if (rc) return rc;
@@ -403,7 +514,7 @@ static int create3d(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdg
 extern "C" {
 
 const char* hdgc_last_error(void) { return g_err.c_str(); }
-const char* hdgc_version(void) { return "hdgconv 0.1 sm_100a fp64"; }
+const char* hdgc_version(void) { return "hdgconv 0.2 sm_100a fp64"; }
 
 int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ctx** out) {
   if (!mesh || !tab || !out) return hdgc_set_err(HDGC_EINVAL, "null argument");
@@ -505,6 +616,7 @@ int hdgc_destroy(hdgc_ctx* c) {
   cudaFree(c->d_sign); cudaFree(c->d_scratch); cudaFree(c->d_scratch2); cudaFree(c->d_modal); cudaFree(c->d_prep); cudaFree(c->d_ftab); cudaFree(c->d_hu); cudaFree(c->d_hw); cudaFree(c->d_hr); cudaFree(c->d_hin);
   cudaFree(c->d_uext); cudaFree(c->d_rn); cudaFree(c->d_sum);
   cudaFree(c->d_dof); cudaFree(c->d_dfac); cudaFree(c->d_inv); cudaFree(c->d_invf); cudaFree(c->d_gl); cudaFree(c->d_rw);
+  cudaFree(c->d_celems); cudaFree(c->d_cminv); cudaFree(c->d_citrans); cudaFree(c->d_cpiola); cudaFree(c->d_cres);
   if (c->h_sum) cudaFreeHost(c->h_sum);
   if (c->blas) cublasDestroy(static_cast<cublasHandle_t>(c->blas));
   delete c;
@@ -533,7 +645,8 @@ int hdgc_apply_w(hdgc_ctx* c, const double* u, const double* inflow, double* r_w
   cudaStream_t st = (cudaStream_t)stream;
   int rc = transfer(c, 0, u, c->d_scratch, st);
   if (rc) return rc;
-  if (c->variant == 0) return elem(c, MODE_APPLY_IT, u, c->d_scratch, inflow, r_w, StageParams(), st);
+  if (c->variant == 0 && c->n_curved == 0)
+    return elem(c, MODE_APPLY_IT, u, c->d_scratch, inflow, r_w, StageParams(), st);
   // sum-factorised: r_V into scratch2, then I^T
   if (!c->d_scratch2 &&
       (rc = hdgc_dev_alloc(c, (void**)&c->d_scratch2, sizeof(double) * (size_t)c->nt * c->nb)))
@@ -739,10 +852,53 @@ int hdgc_mass_inverse(hdgc_ctx* c, double* out, void* stream) {
   return HDGC_OK;
 }
 
+static int maxspeed_affine(hdgc_ctx* c, const double* u, double* out, cudaStream_t st) {
+  HDGC_K_SWITCH(c->k, launch_maxspeed<KK>(c, u, out, st));
+}
+
 int hdgc_max_speed(hdgc_ctx* c, const double* u, double* out_dev, void* stream) {
   if (!c || !u || !out_dev) return hdgc_set_err(HDGC_EINVAL, "null argument");
   if (c->dim == 3) return maxspeed3(c, u, out_dev, (cudaStream_t)stream);
-  HDGC_K_SWITCH(c->k, launch_maxspeed<KK>(c, u, out_dev, (cudaStream_t)stream));
+  int rc = maxspeed_affine(c, u, out_dev, (cudaStream_t)stream);
+  if (rc || c->n_curved == 0) return rc;
+  const int th = 256, work = c->n_curved * c->nqv, nbs1 = c->k * (c->k + 1) / 2;
+  const size_t off_vd = (size_t)c->nb * c->nb + (size_t)nbs1 * c->nb + c->nqv;   // Dims<K>::OFF_VD
+  curved_maxspeed_kernel<<<(work + th - 1) / th, th, 0, (cudaStream_t)stream>>>(
+      c->d_celems, c->n_curved, c->nbs, c->nb + nbs1, c->nqv, c->d_tab + off_vd, c->d_modal, c->d_cpiola,
+      reinterpret_cast<unsigned long long*>(out_dev));
+  CUDA_TRY(cudaGetLastError());
+  return HDGC_OK;
+}
+
+int hdgc_set_curved(hdgc_ctx* c, int32_t n, const int32_t* elems, const double* minv_blocks,
+                    const double* itrans, const double* piola) {
+  if (!c) return hdgc_set_err(HDGC_EINVAL, "null context");
+  if (c->dim != 2) return hdgc_set_err(HDGC_EUNSUP, "curved elements: 2D contexts only");
+  if (c->n_curved) return hdgc_set_err(HDGC_EINVAL, "curved elements already installed on this context");
+  if (n < 0 || n > c->nt) return hdgc_set_err(HDGC_EINVAL, "n_curved=%d out of range", n);
+  if (n == 0) return HDGC_OK;
+  if (!elems || !minv_blocks || !itrans || !piola) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  for (int i = 0; i < n; ++i) {
+    if (elems[i] < 0 || elems[i] >= c->nt) return hdgc_set_err(HDGC_EINVAL, "curved element %d out of range", elems[i]);
+    if (i && elems[i] <= elems[i - 1]) return hdgc_set_err(HDGC_EINVAL, "curved element ids must ascend");
+  }
+  const size_t nbs2 = (size_t)c->nbs * c->nbs, nb2 = (size_t)c->nb * c->nb, pq = (size_t)c->nqv * 4;
+  int rc;
+  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_celems, sizeof(int32_t) * n)) ||
+      (rc = hdgc_dev_alloc(c, (void**)&c->d_cminv, sizeof(double) * n * nbs2)) ||
+      (rc = hdgc_dev_alloc(c, (void**)&c->d_citrans, sizeof(double) * n * nb2)) ||
+      (rc = hdgc_dev_alloc(c, (void**)&c->d_cpiola, sizeof(double) * n * pq)) ||
+      (rc = hdgc_dev_alloc(c, (void**)&c->d_cres, sizeof(double) * n * c->nb)))
+    return rc;
+  CUDA_TRY(cudaMemcpy(c->d_celems, elems, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_cminv, minv_blocks, sizeof(double) * n * nbs2, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_citrans, itrans, sizeof(double) * n * nb2, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_cpiola, piola, sizeof(double) * n * pq, cudaMemcpyHostToDevice));
+  mark_curved_kernel<<<(n + 127) / 128, 128>>>(c->d_celems, n, c->d_minv);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaDeviceSynchronize());
+  c->n_curved = n;
+  return HDGC_OK;
 }
 
 static int ensure_staging(hdgc_ctx* c, bool need_inflow) {

@@ -56,7 +56,8 @@ transfer2d_kernel(const double* __restrict__ tab, const double* __restrict__ pio
 template <int K>
 __global__ void __launch_bounds__(256)
 maxspeed2d_kernel(const double* __restrict__ tab, const double* __restrict__ piola, int nt,
-                  const double* __restrict__ modal, unsigned long long* __restrict__ out) {
+                  const double* __restrict__ modal, const double* __restrict__ minv,
+                  unsigned long long* __restrict__ out) {
   using D = Dims<K>;
   constexpr int NBS = D::NBS, MR = D::NB + D::NBS1, NQV = D::NQV;
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -76,7 +77,7 @@ maxspeed2d_kernel(const double* __restrict__ tab, const double* __restrict__ pio
     const double P00 = __ldg(piola + T), P01 = __ldg(piola + (size_t)nt + T);
     const double P10 = __ldg(piola + 2 * (size_t)nt + T), P11 = __ldg(piola + 3 * (size_t)nt + T);
     const double x = fma(P00, a, P01 * b), y = fma(P10, a, P11 * b);
-    best = sqrt(fma(x, x, y * y));
+    best = __ldg(minv + T) > 0.0 ? sqrt(fma(x, x, y * y)) : 0.0;   // curved: curved_maxspeed_kernel
   }
   for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
@@ -142,7 +143,7 @@ int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st) 
   if (rc) return rc;
   CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
   const long long work = (long long)c->nt * Dims<K>::NQV;
-  maxspeed2d_kernel<K><<<grid_for(work, 256), 256, 0, st>>>(c->d_tab, c->d_piola, c->nt, c->d_modal,
+  maxspeed2d_kernel<K><<<grid_for(work, 256), 256, 0, st>>>(c->d_tab, c->d_piola, c->nt, c->d_modal, c->d_minv,
                                                            reinterpret_cast<unsigned long long*>(out));
   CUDA_TRY(cudaGetLastError());
   return HDGC_OK;

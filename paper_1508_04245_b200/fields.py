@@ -109,33 +109,57 @@ def interpolate_curl(mesh, k: int, sf: StreamFunction, chunk: int = 65536) -> np
         gbq = q2[:, :, None] * gb[:, None, :] + b[:, None, None] * gq2
         curl = np.stack([gbq[:, :, 1], -gbq[:, :, 0]], axis=-1) * qv.weights[:, None, None]
     A_all, B_all = _edge_geometry(mesh)
-    for s in range(0, NT, chunk):
-        sl = slice(s, min(NT, s + chunk))
-        n = sl.stop - sl.start
-        A, Bv = A_all[sl], B_all[sl]
+    t = qe.points
+
+    def rows(A, Bv, X, xq, J, det):
+        """coefficients of n elements from the physical edge points X (n,3,nq,2)
+        and the physical volume points xq (n,p,2) with their J, detJ"""
+        n = A.shape[0]
+        res = np.empty((n, nb))
         psi_a = sf.psi(A[..., 0], A[..., 1])                   # (n, 3)
         psi_b = sf.psi(Bv[..., 0], Bv[..., 1])
-        t = qe.points
-        X = A[:, :, None, :] + t[None, None, :, None] * (Bv - A)[:, :, None, :]   # (n,3,nq,2)
         psi_q = sf.psi(X[..., 0], X[..., 1])                   # (n, 3, nq)
         integ = np.einsum("neq,q,qm->nem", psi_q, qe.weights, dL)
         c = (psi_b[:, :, None] * L1[None, None, :] - psi_a[:, :, None] * L0[None, None, :] - integ)
         c /= elen[None, :, None]
-        out[sl, :3 * (k + 1)] = c.reshape(n, 3 * (k + 1))
+        res[:, :3 * (k + 1)] = c.reshape(n, 3 * (k + 1))
         if n_int:
             # gradient moments: sum_e |e| int (sum_m c_em L_m) q_j dt
             tr = np.einsum("nem,qm->neq", c, Lq)              # normal trace at points
             g = np.einsum("e,neq,q,eqj->nj", elen, tr, qe.weights, qedge)
-            # curl-bubble moments of the pulled-back exact field
-            J = mesh.affine_jac[sl]
-            det = mesh.affine_det[sl]
-            Jinv = mesh.affine_inv[sl]
-            xq = mesh.affine_origin[sl][:, None, :] + np.einsum("ncd,pd->npc", J, qv.points)
+            # curl-bubble moments of the pulled-back exact field u_hat = detJ J^-1 u
             u = sf.velocity(xq[..., 0], xq[..., 1])            # (n, p, 2)
-            uhat = det[:, None, None] * np.einsum("ncd,npd->npc", Jinv, u)
+            adj = np.stack([np.stack([J[..., 1, 1], -J[..., 0, 1]], -1),
+                            np.stack([-J[..., 1, 0], J[..., 0, 0]], -1)], -2)   # detJ J^-1
+            uhat = np.einsum("n...cd,n...d->n...c", adj, u)
             cb = np.einsum("pjc,npc->nj", curl, uhat)
-            out[sl, 3 * (k + 1):] = np.concatenate([g, cb], axis=1)
+            res[:, 3 * (k + 1):] = np.concatenate([g, cb], axis=1)
+        return res
+
+    for s in range(0, NT, chunk):
+        sl = slice(s, min(NT, s + chunk))
+        A, Bv = A_all[sl], B_all[sl]
+        X = A[:, :, None, :] + t[None, None, :, None] * (Bv - A)[:, :, None, :]   # (n,3,nq,2)
+        if n_int:
+            J = mesh.affine_jac[sl]
+            xq = mesh.affine_origin[sl][:, None, :] + np.einsum("ncd,pd->npc", J, qv.points)
+            Jp = np.broadcast_to(J[:, None], (J.shape[0], qv.points.shape[0], 2, 2))
+            det = np.broadcast_to(mesh.affine_det[sl][:, None], Jp.shape[:2])
+        else:
+            xq = Jp = det = None
+        out[sl] = rows(A, Bv, X, xq, Jp, det)
+    ce = _curved(mesh)
+    if ce.size:
+        # curved elements: edge points on the mapped (curved) edges, per-point J
+        X = np.stack([mesh.geometry_batch(ce, B.ref_edge_points(e, t))[0] for e in range(3)], axis=1)
+        xq, Jp, det = mesh.geometry_batch(ce, qv.points) if n_int else (None, None, None)
+        out[ce] = rows(A_all[ce], B_all[ce], X, xq, Jp, det)
     return out
+
+
+def _curved(mesh) -> np.ndarray:
+    f = getattr(mesh, "curved_elements", None)
+    return f() if f is not None and getattr(mesh, "curved_maps", None) else np.zeros(0, dtype=np.int64)
 
 
 def inflow_values(mesh, k: int, sf: StreamFunction) -> np.ndarray:
@@ -147,6 +171,11 @@ def inflow_values(mesh, k: int, sf: StreamFunction) -> np.ndarray:
     a = mesh.vertices[mesh.facet_vertices[bf, 0]]
     b = mesh.vertices[mesh.facet_vertices[bf, 1]]
     X = a[:, None, :] + qf.points[None, :, None] * (b - a)[:, None, :]
+    if _curved(mesh).size:
+        # curved boundary facets: the points on the owner's mapped edge
+        own, loc = mesh.facet_elems[bf, 0], mesh.facet_local[bf, 0]
+        for i in np.nonzero([mesh.is_curved(e) for e in own])[0]:
+            X[i] = mesh.geometry_batch([own[i]], B.ref_edge_points(int(loc[i]), qf.points))[0][0]
     return np.ascontiguousarray(sf.velocity(X[..., 0], X[..., 1]))
 
 
@@ -157,7 +186,14 @@ def transfer_I_host(mesh, k: int, u_loc: np.ndarray) -> np.ndarray:
     nbs = B.nbs_of(k)
     uh = (u_loc @ bdm.coef.T).reshape(-1, 2, nbs)
     P = mesh.affine_jac / mesh.affine_det[:, None, None]
-    return np.einsum("ncd,ndm->ncm", P, uh).reshape(-1, 2 * nbs)
+    w = np.einsum("ncd,ndm->ncm", P, uh).reshape(-1, 2 * nbs)
+    ce = _curved(mesh)
+    if ce.size:
+        # curved elements: element-wise L2 projection
+        from .curved import curved_tables
+        tab = curved_tables(mesh, k)
+        w[ce] = np.einsum("nij,nj->ni", tab["itrans"], u_loc[ce])
+    return w
 
 
 def max_speed_host(mesh, k: int, u_loc: np.ndarray, chunk: int = 65536) -> float:
@@ -171,6 +207,15 @@ def max_speed_host(mesh, k: int, u_loc: np.ndarray, chunk: int = 65536) -> float
         uh = np.einsum("pjd,nj->npd", phi, u_loc[sl])
         P = mesh.affine_jac[sl] / mesh.affine_det[sl, None, None]
         u = np.einsum("ncd,npd->npc", P, uh)
+        sp = np.sqrt((u ** 2).sum(-1))
+        cur = _curved(mesh)
+        if cur.size:
+            sp[np.isin(np.arange(sl.start, sl.stop), cur)] = 0.0     # curved rows: per-point J below
+        best = max(best, float(sp.max()))
+    ce = _curved(mesh)
+    if ce.size:
+        _, J, det = mesh.geometry_batch(ce, q.points)
+        u = np.einsum("npcd,pjd,nj->npc", J, phi, u_loc[ce]) / det[..., None]
         best = max(best, float(np.sqrt((u ** 2).sum(-1)).max()))
     return best
 

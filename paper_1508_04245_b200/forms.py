@@ -167,7 +167,8 @@ def _torch():
 
 
 class ConvectionOperator:
-    """Device context for C^V on one affine mesh and order k.
+    """Device context for C^V on one mesh (affine, or with curved boundary
+    elements) and order k.
 
     Owns the uploaded tables, the on-device geometry (Piola factors J/detJ,
     2/detJ) and the element-owned neighbour codes; compute calls allocate
@@ -230,6 +231,16 @@ class ConvectionOperator:
         self.info = info
         self.n_elements = info.n_elements
         self.n_boundary_facets = info.n_boundary_facets
+        self.curved = None
+        if self.dim == 2 and getattr(mesh, "curved_maps", None):
+            # isoparametric elements along curved boundaries (MESH:555-615): block
+            # mass inverse, L2-projection transfer, per-point Piola
+            from .curved import curved_tables
+            ctab = curved_tables(mesh, self.k)
+            self.curved = ctab
+            n = int(ctab["elems"].size)
+            _lib.check(lib.hdgc_set_curved(h, n, arr(ctab["elems"], np.int32), arr(ctab["minv"]),
+                                           arr(ctab["itrans"]), arr(ctab["piola"])), "hdgc_set_curved")
 
     # -- helpers ---------------------------------------------------------------
 
@@ -441,7 +452,9 @@ class ConvectionOperator:
         return out.cpu().numpy() if host else out
 
     def mass_inverse(self):
-        """(M^V)^{-1} diagonal: 2/detJ per element."""
+        """(M^V)^{-1} diagonal: 2/detJ per element.  On a
+        curved mesh the curved rows hold -(slot + 1); their full blocks are
+        ``self.curved["minv"][slot]`` (PAPER.md:473-475)."""
         torch = _torch()
         lib = _lib.load()
         out = torch.empty(self.n_elements, dtype=torch.float64, device="cuda")

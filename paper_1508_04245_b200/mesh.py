@@ -27,21 +27,53 @@ from __future__ import annotations
 
 import numpy as np
 
-from .basis import REF_EDGES
+from dataclasses import dataclass
 
-__all__ = ["MeshError", "TriMesh", "build_mesh", "generate_structured", "generate_jittered", "load_mesh",
-           "save_mesh"]
+from .basis import REF_EDGES, REF_VERTICES, quad_triangle
+
+__all__ = ["MeshError", "TriMesh", "Circle", "build_mesh", "generate_structured", "generate_jittered",
+           "generate_ring", "curve_boundary", "geometry_map", "load_mesh", "save_mesh"]
 
 
 class MeshError(Exception):
     """Invalid mesh topology or geometry (MESH:18-19)."""
 
 
+@dataclass(frozen=True)
+class Circle:
+    """Circular boundary geometry for curved facets (MESH:23-27)."""
+
+    center: tuple
+    radius: float
+
+
+def lattice(g: int):
+    """Principal lattice exponents/nodes of a degree-g triangle, (i, j) with
+    j outer, i inner — the ordering of the curved-map monomial fit (MESH:48-50)."""
+    return [(i, j) for j in range(g + 1) for i in range(g + 1 - j)]
+
+
+def _monomials(exps, pts, deriv=False):
+    """x^i y^j at pts (n, 2) -> (n, nm); with deriv also d/dx, d/dy -> (n, nm, 2)."""
+    pts = np.atleast_2d(np.asarray(pts, dtype=float))
+    e = np.asarray(exps, dtype=np.int64).reshape(-1, 2)
+    x, y = pts[:, :1], pts[:, 1:2]
+    ei, ej = e[None, :, 0], e[None, :, 1]
+    val = x ** ei * y ** ej
+    if not deriv:
+        return val
+    gx = np.where(ei > 0, ei * x ** np.maximum(ei - 1, 0) * y ** ej, 0.0)
+    gy = np.where(ej > 0, ej * x ** ei * y ** np.maximum(ej - 1, 0), 0.0)
+    return val, np.stack([gx, gy], axis=-1)
+
+
 class TriMesh:
-    """Immutable affine triangulation with oriented facets."""
+    """Immutable triangulation with oriented facets: affine elements, plus
+    optional degree-g isoparametric maps on the elements along curved
+    boundary labels (``curved_maps``, MESH:94-150, 555-615)."""
 
     def __init__(self, vertices, triangles, facet_vertices, facet_elems, facet_local,
-                 facet_flip, facet_labels=None):
+                 facet_flip, facet_labels=None, geometry_order=1, curved_maps=None, curved_geometry=None):
         self.vertices = np.ascontiguousarray(vertices, dtype=float)
         self.triangles = np.ascontiguousarray(triangles, dtype=np.int64)
         self.facet_vertices = np.ascontiguousarray(facet_vertices, dtype=np.int64)
@@ -49,7 +81,9 @@ class TriMesh:
         self.facet_local = np.ascontiguousarray(facet_local, dtype=np.int64)
         self.facet_flip = np.ascontiguousarray(facet_flip, dtype=bool)
         self.facet_labels = dict(facet_labels or {})
-        self.curved_maps = {}
+        self.geometry_order = int(geometry_order)
+        self.curved_maps = dict(curved_maps or {})            # elem -> (2, n_mono) monomial coefficients
+        self.curved_geometry = dict(curved_geometry or {})    # label -> Circle
         self.n_elements = len(self.triangles)
         self.n_facets = len(self.facet_vertices)
 
@@ -102,10 +136,52 @@ class TriMesh:
         return float(self.facet_h.min())
 
     def total_area(self) -> float:
-        return float(0.5 * self.affine_det.sum())
+        area = float(0.5 * self.affine_det.sum())
+        if self.curved_maps:
+            ce = self.curved_elements()
+            q = quad_triangle(max(2 * self.geometry_order, 2))
+            _, _, det = self.geometry_batch(ce, q.points)
+            area += float((det @ q.weights).sum() - 0.5 * self.affine_det[ce].sum())
+        return area
 
     def is_curved(self, elem) -> bool:
-        return False
+        return int(elem) in self.curved_maps
+
+    def curved_elements(self) -> np.ndarray:
+        """Sorted ids of the elements carrying a curved map."""
+        return np.array(sorted(self.curved_maps), dtype=np.int64)
+
+    def curved_facets(self) -> np.ndarray:
+        """Facets on a curved boundary label (MESH:246-252)."""
+        return np.array(sorted(f for f, lab in self.facet_labels.items() if lab in self.curved_geometry),
+                        dtype=np.int64)
+
+    def facets_with_label(self, label) -> np.ndarray:
+        return np.array(sorted(f for f, lab in self.facet_labels.items() if lab == label), dtype=np.int64)
+
+    def geometry_batch(self, elems, ref_pts):
+        """x (n, p, 2), J (n, p, 2, 2) and detJ (n, p) of the elements ``elems``
+        at the reference points: the curved map where one is attached, the
+        affine map otherwise (vectorised MESH:254-278)."""
+        elems = np.asarray(elems, dtype=np.int64).reshape(-1)
+        pts = np.atleast_2d(np.asarray(ref_pts, dtype=float))
+        n, p = elems.size, pts.shape[0]
+        J = np.broadcast_to(self.affine_jac[elems][:, None], (n, p, 2, 2)).copy()
+        x = self.affine_origin[elems][:, None, :] + np.einsum("ncd,pd->npc", self.affine_jac[elems], pts)
+        cur = np.array([int(e) in self.curved_maps for e in elems], dtype=bool)
+        if cur.any():
+            val, grad = _monomials(lattice(self.geometry_order), pts, deriv=True)
+            cm = np.stack([self.curved_maps[int(e)] for e in elems[cur]])      # (nc, 2, nm)
+            x[cur] = np.einsum("ncm,pm->npc", cm, val)
+            J[cur] = np.einsum("ncm,pmd->npcd", cm, grad)
+        det = J[..., 0, 0] * J[..., 1, 1] - J[..., 0, 1] * J[..., 1, 0]
+        return x, J, det
+
+    def geometry_map(self, elem, ref_pts):
+        """(x, J, detJ) of one element at reference points, shapes (n,2),
+        (n,2,2), (n,) — the reference's ``Mesh.geometry_map`` (MESH:254-278)."""
+        x, J, det = self.geometry_batch([elem], ref_pts)
+        return x[0], J[0], det[0]
 
     # -- adjacency views used by the device context --------------------------
 
@@ -243,6 +319,125 @@ def generate_jittered(n, amplitude=0.2, seed=0, labels=("left", "right", "bottom
     verts = verts.copy()
     verts[interior] += jit[interior]
     return build_mesh(verts, tris, _structured_markers(n, n, labels))
+
+
+def geometry_map(mesh, elem, ref_pts):
+    """Module-level alias of ``TriMesh.geometry_map`` (MESH:638-640)."""
+    return mesh.geometry_map(elem, ref_pts)
+
+
+def generate_ring(circle: Circle, rect, n_theta, n_layers, theta_offset=0.0, radial_fractions=None,
+                  inner_label="obstacle", outer_labels=("left", "right", "bottom", "top")) -> TriMesh:
+    """O-grid between a circle and an enclosing rectangle, 2 n_theta n_layers
+    triangles (restates MESH:381-443): ray i at angle theta_offset + 2 pi i /
+    n_theta runs from the circle to the rectangle, layer s at radial fraction
+    s; cell (i, j) -> triangles (a, b, c), (a, c, d).  Inner chords carry
+    ``inner_label`` (curve them with ``curve_boundary``); each outer segment
+    must lie on one rectangle side."""
+    (cx, cy), r = circle.center, circle.radius
+    x0, y0, x1, y1 = rect
+    th = theta_offset + 2.0 * np.pi * np.arange(n_theta) / n_theta
+    d = np.stack([np.cos(th), np.sin(th)], axis=1)
+    # distance along each ray to the rectangle: smallest positive hit
+    with np.errstate(divide="ignore", invalid="ignore"):
+        tx = np.where(d[:, 0] > 1e-14, (x1 - cx) / d[:, 0], np.where(d[:, 0] < -1e-14, (x0 - cx) / d[:, 0], np.inf))
+        ty = np.where(d[:, 1] > 1e-14, (y1 - cy) / d[:, 1], np.where(d[:, 1] < -1e-14, (y0 - cy) / d[:, 1], np.inf))
+    hit = np.minimum(np.where(tx > 0, tx, np.inf), np.where(ty > 0, ty, np.inf))
+    c = np.array([cx, cy])
+    inner = c + r * d
+    outer = c + hit[:, None] * d
+    fr = np.linspace(0.0, 1.0, n_layers + 1) if radial_fractions is None else np.asarray(radial_fractions, float)
+    verts = np.concatenate([inner * (1.0 - s) + outer * s for s in fr], axis=0)
+    vid = lambda i, j: j * n_theta + (i % n_theta)
+    tris = []
+    for j in range(n_layers):
+        for i in range(n_theta):
+            a, b, cc, dd = vid(i, j), vid(i + 1, j), vid(i + 1, j + 1), vid(i, j + 1)
+            tris += [(a, b, cc), (a, cc, dd)]
+    markers = {tuple(sorted((vid(i, 0), vid(i + 1, 0)))): inner_label for i in range(n_theta)}
+    left, right, bottom, top = outer_labels
+    tol = 1e-10 * max(x1 - x0, y1 - y0)
+    for i in range(n_theta):
+        a, b = vid(i, n_layers), vid(i + 1, n_layers)
+        pa, pb = verts[a], verts[b]
+        for lab, ax, val in ((left, 0, x0), (right, 0, x1), (bottom, 1, y0), (top, 1, y1)):
+            if abs(pa[ax] - val) < tol and abs(pb[ax] - val) < tol:
+                markers[tuple(sorted((a, b)))] = lab
+                break
+        else:
+            raise MeshError("outer ring segment spans a rectangle corner; "
+                            "choose theta_offset/n_theta so rays hit corners")
+    return build_mesh(verts, np.array(tris, dtype=np.int64), markers)
+
+
+def _on_edge(ea, eb, pt, tol=1e-12):
+    """Parameter s in [0, 1] of pt on the segment ea -> eb, or None."""
+    d, w = eb - ea, pt - ea
+    if abs(d[0] * w[1] - d[1] * w[0]) > tol:
+        return None
+    s = float(np.dot(w, d) / np.dot(d, d))
+    return min(max(s, 0.0), 1.0) if -tol <= s <= 1.0 + tol else None
+
+
+def curve_boundary(mesh: TriMesh, label, geometry: Circle, g: int) -> TriMesh:
+    """Attach degree-g isoparametric maps to the owners of the ``label``
+    facets (restates MESH:555-615): the degree-g lattice of each owner is
+    placed at its affine position, the nodes on the labelled edge are moved
+    onto the circle at equal angle steps between the edge's end points, and
+    the map x(x_hat) = sum_m c_m x_hat^i y_hat^j interpolates the nodes.
+    Interior edges keep their affine lattice nodes, so they stay straight
+    and are parametrised exactly as in the neighbour's affine map."""
+    if g < 1:
+        raise MeshError("geometry order must be >= 1")
+    if not isinstance(geometry, Circle):
+        raise MeshError("only circular boundary geometry is supported")
+    facets = mesh.facets_with_label(label)
+    if facets.size == 0:
+        raise MeshError(f"no facets labeled {label!r}")
+    c = np.asarray(geometry.center, dtype=float)
+    r = float(geometry.radius)
+    for f in facets:
+        for v in mesh.facet_vertices[f]:
+            if abs(np.linalg.norm(mesh.vertices[v] - c) - r) > 1e-8 * r:
+                raise MeshError(f"facet {f} endpoint not on the circle")
+    geom = dict(mesh.curved_geometry)
+    geom[label] = geometry
+
+    def rebuild(order, maps):
+        return TriMesh(mesh.vertices, mesh.triangles, mesh.facet_vertices, mesh.facet_elems, mesh.facet_local,
+                       mesh.facet_flip, mesh.facet_labels, geometry_order=order, curved_maps=maps,
+                       curved_geometry=geom)
+
+    if g == 1:
+        return rebuild(1, {})
+    exps = lattice(g)
+    nodes = np.array([(i / g, j / g) for i, j in exps])
+    V = _monomials(exps, nodes)
+    owned = {}
+    for f in facets:
+        owned.setdefault(int(mesh.facet_elems[f, 0]), []).append(int(f))
+    maps = dict(mesh.curved_maps)
+    for e, fl in owned.items():
+        corners = mesh.vertices[mesh.triangles[e]]
+        phys = corners[0] + nodes @ np.stack([corners[1] - corners[0], corners[2] - corners[0]])
+        for f in fl:
+            loc = int(np.nonzero(mesh.elem_facets[e] == f)[0][0])
+            la, lb = REF_EDGES[loc]
+            ta = np.arctan2(*(corners[la] - c)[::-1])
+            tb = np.arctan2(*(corners[lb] - c)[::-1])
+            dth = (tb - ta + np.pi) % (2.0 * np.pi) - np.pi      # short arc
+            for m, pt in enumerate(nodes):
+                s = _on_edge(REF_VERTICES[la], REF_VERTICES[lb], pt)
+                if s is not None:
+                    phys[m] = c + r * np.array([np.cos(ta + s * dth), np.sin(ta + s * dth)])
+        maps[e] = np.linalg.solve(V, phys).T.copy()               # (2, n_mono)
+    out = rebuild(g, maps)
+    q = quad_triangle(max(4, 2 * g + 2))
+    _, _, det = out.geometry_batch(out.curved_elements(), q.points)
+    if np.any(det <= 0):
+        raise MeshError(f"curved element {int(out.curved_elements()[np.nonzero((det <= 0).any(1))[0][0]])} "
+                        "has nonpositive Jacobian")
+    return out
 
 
 # ---------------------------------------------------------------------------
