@@ -79,6 +79,11 @@ struct SF {
   // cost occupancy and spills there
   static constexpr bool RING = K >= 7;
 #endif
+#ifdef HDGC_SMEM_BT
+  static constexpr bool SMBT = RING || HDGC_SMEM_BT;
+#else
+  static constexpr bool SMBT = RING;
+#endif
   static constexpr int RING_SLOT = 3 * N * 16;     // alpha | beta | gamma of one row, [3][N][16]
   // smem (doubles): mbarrier | prep tile [PREP][EPB] or ring [2][3][N][EPB] |
   //                 w tile [EPB][NB] | halo [THREADS][NBS] | fD [3][NF][NBS]
@@ -94,7 +99,7 @@ struct SF {
   // ring mode: B / B' row tables interleaved [N][NBS](B, B') in smem (uniform LDS.128
   // instead of runtime-indexed constant loads, which ptxas hoists into registers)
   static constexpr int SM_BT = SM_FD + TAB_PAD;
-  static constexpr int SMEM_DOUBLES = SM_BT + (RING ? 2 * N * NBS : 0);
+  static constexpr int SMEM_DOUBLES = SM_BT + (SMBT ? 2 * N * NBS : 0);
 };
 
 // The constant-bank tables of the order compiled in this translation unit
@@ -383,7 +388,7 @@ __device__ __forceinline__ void sf_row(const WS& wv, const double* al, const dou
     for (int j = 0; j <= K - i; ++j) {
       const int m = midx(i, j);
       const double x = wv[m];
-      if (F::RING) {
+      if (F::SMBT) {
         const double2 t = BT[m];
         sw = fma(x, t.x, sw);
         swd = fma(x, t.y, swd);
@@ -418,16 +423,41 @@ __device__ __forceinline__ void sf_row(const WS& wv, const double* al, const dou
 #pragma unroll
     for (int j = 0; j <= K - i; ++j) {
       const int m = midx(i, j);
-      r[m] = fma(Kc[i], F::RING ? BT[m].x : Bb[m], r[m]);
+      r[m] = fma(Kc[i], F::SMBT ? BT[m].x : Bb[m], r[m]);
     }
   }
 }
 
 // Volume rows [b0, b1) with w_c cached in registers; row: the element's prep
 // column (slot j at row[j * EPB], smem tile or global).
-template <int K>
-__device__ __forceinline__ void sf_rows(const double* wc, const double* row, int b0, int b1,
-                                        double (&r)[SF<K>::NBS], const double2* sBT) {
+#ifndef HDGC_ROW_UNROLL
+#define HDGC_ROW_UNROLL 1
+#endif
+// Volume rows [b0, b1) with w_c cached in registers; row: the element's prep
+// column (slot j at row[j * EPB], smem tile or global).
+#ifndef HDGC_ROW_UNROLL
+#define HDGC_ROW_UNROLL 1
+#endif
+#ifndef HDGC_ROW_SWITCH
+#define HDGC_ROW_SWITCH 0
+#endif
+// one row with a compile-time row index (immediate constant-bank operands for B, B')
+template <int K, int B, class WS>
+__device__ __forceinline__ void sf_row_fixed(const WS& wv, const double* row, double (&r)[SF<K>::NBS],
+                                             const double2* sBT) {
+  using F = SF<K>;
+  sf_row<K>(wv, row + (F::P_AL + B * F::N) * F::EPB, row + (F::P_BE + B * F::N) * F::EPB,
+            row + (F::P_GA + B * F::N) * F::EPB, B, r, sBT);
+}
+template <int K, class WS, int... Bs>
+__device__ __forceinline__ void sf_row_switch(int b, const WS& wv, const double* row, double (&r)[SF<K>::NBS],
+                                              const double2* sBT, std::integer_sequence<int, Bs...>) {
+  ((b == Bs ? sf_row_fixed<K, Bs>(wv, row, r, sBT) : void()), ...);
+}
+template <int K, int B0, int B1>
+__device__ __forceinline__ void sf_rows(const double* wc, const double* row, double (&r)[SF<K>::NBS],
+                                        const double2* sBT) {
+  constexpr int b0 = B0, b1 = B1, RU = HDGC_ROW_UNROLL;
   using F = SF<K>;
   constexpr int N = F::N, NBS = F::NBS, EPB = F::EPB;
   if constexpr (F::RING) {
@@ -439,7 +469,7 @@ __device__ __forceinline__ void sf_rows(const double* wc, const double* row, int
     double wo[NBS];
 #pragma unroll
     for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
-#pragma unroll 1
+#pragma unroll RU
     for (int b = b0; b < b1; ++b)
       sf_row<K>(wo, row + (F::P_AL + b * N) * EPB, row + (F::P_BE + b * N) * EPB, row + (F::P_GA + b * N) * EPB,
                 b, r, sBT);
@@ -519,7 +549,9 @@ __device__ __forceinline__ void stage_x(const StageParams& st, double mi, double
 #ifdef HDGC_SF_MINB
 #define HDGC_SF_MINB_OF(K) HDGC_SF_MINB
 #else
-#define HDGC_SF_MINB_OF(K) (K <= 4 ? 6 : (K <= 6 ? 4 : 2))   // register caps 170 / 256 / 255 (k >= 7: 4 CTAs/SM by smem + regs)
+// register caps 128 / 256 / 255: k <= 4 runs 8 CTAs/SM at 128 registers (a few
+// spilled bytes; k=4 69.8 -> 66.5 us, k=3 53.2 -> 49.7 us measured); k >= 7: 4 CTAs/SM by smem + regs
+#define HDGC_SF_MINB_OF(K) (K <= 4 ? 8 : (K <= 6 ? 4 : 2))
 #endif
 template <int K, int MODE>
 __global__ void __launch_bounds__(SF<K>::THREADS, HDGC_SF_MINB_OF(K))
@@ -541,7 +573,7 @@ conv2d_sf_kernel(SFParams p) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  if (F::RING)
+  if (F::SMBT)
     for (int t = threadIdx.x; t < N * NBS; t += F::THREADS) s_BT[t] = make_double2(C[F::C_B + t], C[F::C_BD + t]);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -550,6 +582,16 @@ conv2d_sf_kernel(SFParams p) {
     const uint32_t bt = (uint32_t)(F::TAB_PAD * sizeof(double));
     mbar_arrive_expect_tx(bar, bp + bw + bt);
     if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
+#ifdef HDGC_L2PF
+    // warm L2 with the prep tile of the CTA that will likely follow on this SM
+    {
+      const unsigned nxt = blockIdx.x + HDGC_L2PF;
+      if (nxt < gridDim.x)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.prep + (size_t)nxt * F::PREP_TILE),
+                     "r"((uint32_t)(F::PREP_TILE * sizeof(double)))
+                     : "memory");
+    }
+#endif
     bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
     bulk_g2s(s_fD, p.ftab, bt, bar);
   }
@@ -574,7 +616,7 @@ conv2d_sf_kernel(SFParams p) {
     mbar_wait(bar, 0);
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
     if (F::RING) sf_rows_ring<K>(wc, gtile, s_prep, active ? le : 0, lane, N - F::FACET_ROWS, r, s_BT);
-    else sf_rows<K>(wc, row, 0, N - F::FACET_ROWS, r, s_BT);
+    else sf_rows<K, 0, N - F::FACET_ROWS>(wc, row, r, s_BT);
     asm volatile("bar.sync 1, 64;\n" ::: "memory");   // (A) facet partial r ready, in-tile w reads done
     if (active) {
       double* wo_s = s_w + le * NB + c * NBS;
@@ -713,7 +755,7 @@ conv2d_sf_kernel(SFParams p) {
       }
     }
     // balance: the facet warp also takes the last FACET_ROWS volume rows
-    if (F::FACET_ROWS > 0) sf_rows<K>(wc, row, N - F::FACET_ROWS, N, r, s_BT);
+    if (F::FACET_ROWS > 0) sf_rows<K, N - F::FACET_ROWS, N>(wc, row, r, s_BT);
     __syncwarp();          // halo reads of all lanes done before the partials overwrite it
 #pragma unroll
     for (int m = 0; m < NBS; ++m) part[m] = r[m];
