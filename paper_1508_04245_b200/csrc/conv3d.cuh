@@ -90,8 +90,11 @@ __global__ void geometry3d_kernel(const double* __restrict__ V, const int64_t* _
                                   double* __restrict__ sgn, int* __restrict__ bad);
 
 #ifdef HDGC_ORDER3   // kernels: only in the per-order translation units
+#ifndef HDGC_3D_SMEM_R
+#define HDGC_3D_SMEM_R 1   // w_c and the volume accumulators r in smem, registers for the sum-factorisation state
+#endif
 #ifndef HDGC_3D_MINB
-#define HDGC_3D_MINB 2
+#define HDGC_3D_MINB (HDGC_3D_SMEM_R ? 4 : 2)   // 168 / 255 registers: 4 / 2 CTAs (12 / 6 warps) per SM (k=3: 1221 us vs 2014 us)
 #endif
 struct Prep3Params {
   const double* __restrict__ tab;
@@ -201,14 +204,21 @@ conv3d_kernel(Conv3Params p) {
   double* s_wo = sm3 + D::RTAB;          // [NBS][96]
   double* s_wn = s_wo + NBS * 96;        // [NBS][96]
   for (int i = threadIdx.x; i < D::RTAB; i += blockDim.x) s_R[i] = __ldg(p.rtab + i);
-  double wo[NBS], r[NBS];
+  constexpr bool SR = HDGC_3D_SMEM_R;
+  // SR: w_c from smem (s_wo) and the volume accumulators in smem (s_wn doubles as
+  // s_r until the face loop), so the sum-factorisation state fits in 136 registers
+  double* s_r = s_wn;
+  double wo[SR ? 1 : NBS], r[NBS];
 #pragma unroll
   for (int m = 0; m < NBS; ++m) {
-    wo[m] = __ldg(p.w + (size_t)T * NB + c * NBS + m);
-    s_wo[m * 96 + threadIdx.x] = wo[m];
-    r[m] = 0.0;
+    const double x = __ldg(p.w + (size_t)T * NB + c * NBS + m);
+    if constexpr (!SR) wo[m] = x;
+    s_wo[m * 96 + threadIdx.x] = x;
+    if constexpr (SR) s_r[m * 96 + threadIdx.x] = 0.0;
+    else r[m] = 0.0;
   }
   __syncthreads();
+  auto W = [&](int m) -> double { if constexpr (SR) return s_wo[m * 96 + threadIdx.x]; else return wo[m]; };
   // ---- volume, sum-factorised over the collapsed rule (c outer, b, a inner):
   //   G_ij(c) = sum_l w_ijl C_ijl(c),  H_i(b,c) = sum_j G_ij(c) B_ij(b),
   //   w(a,b,c) = sum_i A_i(a) H_i(b,c)  (and the a-, b-, c-derivatives),
@@ -230,8 +240,9 @@ conv3d_kernel(Conv3Params p) {
 #pragma unroll
           for (int l = 0; l <= K - i - j; ++l) {
             const int m = midx3(i, j, l);
-            s0 = fma(wo[m], Cc[m], s0);
-            s1 = fma(wo[m], Ccd[m], s1);
+            const double x = W(m);
+            s0 = fma(x, Cc[m], s0);
+            s1 = fma(x, Ccd[m], s1);
           }
           G[pidx(i, j)] = s0;
           Gc[pidx(i, j)] = s1;
@@ -287,9 +298,18 @@ conv3d_kernel(Conv3Params p) {
 #pragma unroll
           for (int l = 0; l <= K - i - j; ++l) {
             const int m = midx3(i, j, l);
-            r[m] = fma(K2[pidx(i, j)], Cc[m], r[m]);
+            if constexpr (SR) {
+              double* rp = s_r + m * 96 + threadIdx.x;
+              *rp = fma(K2[pidx(i, j)], Cc[m], *rp);
+            } else {
+              r[m] = fma(K2[pidx(i, j)], Cc[m], r[m]);
+            }
           }
     }
+  }
+  if constexpr (SR) {
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) r[m] = s_r[m * 96 + threadIdx.x];   // own column only: no barrier needed
   }
   // ---- faces: per-lane work list of inflow faces (the warp runs max_lane(count)
   //      iterations).  Traces are handled in the face's own P_k basis: the
@@ -368,7 +388,7 @@ conv3d_kernel(Conv3Params p) {
   if (MODE == MODE_SUBSTEP) {
     const double cm = p.st.c * __ldg(p.minv + T);
 #pragma unroll
-    for (int m = 0; m < NBS; ++m) og[m] = fma(cm, r[m], wo[m]);
+    for (int m = 0; m < NBS; ++m) og[m] = fma(cm, r[m], W(m));
   } else if (MODE == MODE_STAGE) {
     const double mi = __ldg(p.minv + T);
     const double cm = p.st.c * mi;
@@ -379,8 +399,9 @@ conv3d_kernel(Conv3Params p) {
 #pragma unroll
       for (int m = 0; m < NBS; ++m) {
         const double xv = __ldg(xg + m);
-        og[m] = fma(p.st.b, xv, fma(cm, r[m], p.st.a * wo[m]));
-        const double res = fma(tm, r[m], xv - wo[m]);
+        const double wm = W(m);
+        og[m] = fma(p.st.b, xv, fma(cm, r[m], p.st.a * wm));
+        const double res = fma(tm, r[m], xv - wm);
         acc = fma(res, res, acc);
       }
       if (p.st.rn) p.st.rn[3 * (size_t)T + c] = acc;
