@@ -39,9 +39,15 @@ struct Dims3 {
   static constexpr int OFF_FD = OFF_FL + NF * NFD;                   // [4][NF][NBS]
   static constexpr int OFF_FLEN = OFF_FD + 4 * NF * NBS;             // [4]
   static constexpr int TAB = OFF_FLEN + 4;
-  static constexpr int PREP = 4 * NQ + 4 * NF + 1;                   // + inflow-face bitmask slot
+  static constexpr int NSYM = NFD * (NFD + 1) / 2;                   // upper triangle of a face matrix
+  static constexpr int P_MASK = 4 * NQ + 4 * NF;                     // inflow-face bitmask slot
+  static constexpr int P_S = P_MASK + 1;                             // face inflow matrices S_f [4][NSYM]
+  static constexpr int PREP = P_S + 4 * NSYM;
   static constexpr int NFP = NF + (NF & 1);                          // face points padded (smem table)
-  static constexpr int RTAB = 4 * NFD * NBS;                         // face trace maps R[f][n][m]
+  // face trace maps R[f][n][m] in smem with an odd per-face stride: lanes on
+  // different faces hit disjoint bank pairs (the k=3 stride 200 would alias f, f+2)
+  static constexpr int RSTR = (NFD * NBS) | 1;
+  static constexpr int RTAB = 4 * RSTR;
   static constexpr int SMEM = (RTAB + 2 * NBS * 96) * 8;             // + own / neighbour w columns
   static constexpr int EPB = 32;                                     // elements per CTA
   static constexpr int THREADS = 3 * EPB;                            // one warp per component
@@ -120,20 +126,33 @@ prep3d_kernel(Prep3Params p) {
   // inflow weights from the face dofs (first 4*NFD dofs, face-major) and the
   // bitmask of faces with at least one inflow point
   unsigned fmask = 0;
+  const double* D2 = c_sf3d + SF3<K>::C_D2;
 #pragma unroll 1
   for (int f = 0; f < 4; ++f) {
     const double len = __ldg(tab + D::OFF_FLEN + f);
-#pragma unroll 1
+    double sv[NF];
+#pragma unroll
     for (int q = 0; q < NF; ++q) {
       double a = 0.0;
 #pragma unroll
       for (int m = 0; m < NFD; ++m) a = fma(x[f * NFD + m], __ldg(tab + D::OFF_FL + q * NFD + m), a);
       const double F = sg * a * len;
-      p.prep[(size_t)(4 * NQ + f * NF + q) * nt + T] = F < 0.0 ? __ldg(tab + D::OFF_FW + q) * F : 0.0;
+      sv[q] = F < 0.0 ? __ldg(tab + D::OFF_FW + q) * F : 0.0;
+      p.prep[(size_t)(4 * NQ + f * NF + q) * nt + T] = sv[q];
       if (F < 0.0) fmask |= 1u << f;
     }
+    // face inflow matrix S_f[n][n2] = sum_q s_q D2_n(q) D2_n2(q), upper triangle row-major
+#pragma unroll 1
+    for (int n = 0; n < NFD; ++n)
+#pragma unroll 1
+      for (int n2 = n; n2 < NFD; ++n2) {
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q < NF; ++q) a = fma(sv[q] * D2[q * NFD + n], D2[q * NFD + n2], a);
+        p.prep[(size_t)(D::P_S + f * D::NSYM + n * NFD - n * (n - 1) / 2 + (n2 - n)) * nt + T] = a;
+      }
   }
-  p.prep[(size_t)(4 * NQ + 4 * NF) * nt + T] = (double)fmask;
+  p.prep[(size_t)D::P_MASK * nt + T] = (double)fmask;
   double uh[NB];
 #pragma unroll 1
   for (int i = 0; i < NB; ++i) {
@@ -203,7 +222,10 @@ conv3d_kernel(Conv3Params p) {
   double* s_R = sm3;                     // [4][NFD][NBS]
   double* s_wo = sm3 + D::RTAB;          // [NBS][96]
   double* s_wn = s_wo + NBS * 96;        // [NBS][96]
-  for (int i = threadIdx.x; i < D::RTAB; i += blockDim.x) s_R[i] = __ldg(p.rtab + i);
+  for (int i = threadIdx.x; i < 4 * D::NFD * NBS; i += blockDim.x) {
+    const int f = i / (D::NFD * NBS);
+    s_R[f * D::RSTR + (i - f * D::NFD * NBS)] = __ldg(p.rtab + i);
+  }
   constexpr bool SR = HDGC_3D_SMEM_R;
   // SR: w_c from smem (s_wo) and the volume accumulators in smem (s_wn doubles as
   // s_r until the face loop), so the sum-factorisation state fits in 136 registers
@@ -252,6 +274,16 @@ conv3d_kernel(Conv3Params p) {
       for (int ib = 0; ib < N; ++ib) {
         const double* Bb = Cs + S::C_B + ib * NPAIR;
         const double* Bbd = Cs + S::C_BD + ib * NPAIR;
+        const size_t q0 = (size_t)(ic * N + ib) * N;
+        // the row's flux-form coefficients, all issued before the H contraction
+        double pal[N], pbe[N], pga[N], pde[N];
+#pragma unroll
+        for (int ia = 0; ia < N; ++ia) {
+          pal[ia] = __ldg(p.prep + (q0 + ia) * nt + T);
+          pbe[ia] = __ldg(p.prep + (NQ + q0 + ia) * nt + T);
+          pga[ia] = __ldg(p.prep + (2 * NQ + q0 + ia) * nt + T);
+          pde[ia] = __ldg(p.prep + (3 * NQ + q0 + ia) * nt + T);
+        }
         double H[NE], Hb[NE], Hc[NE], K1[NE];
 #pragma unroll
         for (int i = 0; i <= K; ++i) {
@@ -265,7 +297,6 @@ conv3d_kernel(Conv3Params p) {
           }
           H[i] = h; Hb[i] = hb; Hc[i] = hc; K1[i] = 0.0;
         }
-        const size_t q0 = (size_t)(ic * N + ib) * N;
 #pragma unroll
         for (int ia = 0; ia < N; ++ia) {
           double v = 0.0, va = 0.0, vb = 0.0, vc = 0.0;
@@ -277,12 +308,7 @@ conv3d_kernel(Conv3Params p) {
             vb = fma(Ai, Hb[i], vb);
             vc = fma(Ai, Hc[i], vc);
           }
-          const size_t q = q0 + ia;
-          const double al = __ldg(p.prep + q * nt + T);
-          const double be = __ldg(p.prep + (NQ + q) * nt + T);
-          const double ga = __ldg(p.prep + (2 * NQ + q) * nt + T);
-          const double de = __ldg(p.prep + (3 * NQ + q) * nt + T);
-          const double g = fma(al, va, fma(be, vb, fma(ga, vc, de * v)));
+          const double g = fma(pal[ia], va, fma(pbe[ia], vb, fma(pga[ia], vc, pde[ia] * v)));
 #pragma unroll
           for (int i = 0; i <= K; ++i) K1[i] = fma(g, Cs[S::C_A + ia * NE + i], K1[i]);
         }
@@ -322,7 +348,7 @@ conv3d_kernel(Conv3Params p) {
     using S = SF3<K>;
     constexpr int NFD = D::NFD;
     const double* D2 = c_sf3d + S::C_D2;
-    unsigned fm = active ? (unsigned)__ldg(p.prep + (size_t)(4 * NQ + 4 * NF) * nt + T) : 0u;
+    unsigned fm = active ? (unsigned)__ldg(p.prep + (size_t)D::P_MASK * nt + T) : 0u;
     if (p.inflow == nullptr) {
 #pragma unroll
       for (int f = 0; f < 4; ++f)
@@ -348,8 +374,8 @@ conv3d_kernel(Conv3Params p) {
         for (int m = 0; m < NBS; ++m) s_wn[m * 96 + threadIdx.x] = 0.0;
         if (on) infl = p.inflow + (size_t)(-1 - code) * NF * 3 + c;
       }
-      const double* Rf = s_R + f * NFD * NBS;
-      const double* Rn = s_R + f2 * NFD * NBS;
+      const double* Rf = s_R + f * D::RSTR;
+      const double* Rn = s_R + f2 * D::RSTR;
       double dl[NFD];
 #pragma unroll
       for (int n = 0; n < NFD; ++n) dl[n] = 0.0;
@@ -359,20 +385,33 @@ conv3d_kernel(Conv3Params p) {
 #pragma unroll
         for (int n = 0; n < NFD; ++n) dl[n] = fma(wnm, Rn[n * NBS + m], fma(-wm, Rf[n * NBS + m], dl[n]));
       }
+      // rho_n = sum_q s_q J(q) D2_n(q) with J = sum_n' dl_n' D2_n' (+ inflow data):
+      // the velocity-only part is the frozen face matrix S_f[n][n'] = sum_q s_q D2_n D2_n'
+      // (prep), so rho = S_f dl — NSYM independent loads instead of a dependent
+      // loop over the NF face points
       double rho[NFD];
+      {
+        const double* Sf = p.prep + (size_t)(D::P_S + f * D::NSYM) * nt + T;
 #pragma unroll
-      for (int n = 0; n < NFD; ++n) rho[n] = 0.0;
-      const double* sf = p.prep + (size_t)(4 * NQ + f * NF) * nt + T;
-#pragma unroll 2
-      for (int q = 0; q < NF; ++q) {
-        const double sq = on ? __ldg(sf + (size_t)q * nt) : 0.0;
-        double J = 0.0;
+        for (int n = 0; n < NFD; ++n) rho[n] = 0.0;
 #pragma unroll
-        for (int n = 0; n < NFD; ++n) J = fma(dl[n], D2[q * NFD + n], J);
-        if (infl != nullptr && sq != 0.0) J += __ldg(infl + 3 * q);
-        const double sj = sq * J;
+        for (int n = 0; n < NFD; ++n)
 #pragma unroll
-        for (int n = 0; n < NFD; ++n) rho[n] = fma(sj, D2[q * NFD + n], rho[n]);
+          for (int n2 = n; n2 < NFD; ++n2) {
+            const double sv = on ? __ldg(Sf + (size_t)(n * NFD - n * (n - 1) / 2 + (n2 - n)) * nt) : 0.0;
+            rho[n] = fma(sv, dl[n2], rho[n]);
+            if (n2 != n) rho[n2] = fma(sv, dl[n], rho[n2]);
+          }
+      }
+      if (infl != nullptr) {
+        // boundary face with exterior data: + sum_q s_q g(q) D2_n(q)
+        const double* sf = p.prep + (size_t)(4 * NQ + f * NF) * nt + T;
+#pragma unroll 1
+        for (int q = 0; q < NF; ++q) {
+          const double sg = __ldg(sf + (size_t)q * nt) * __ldg(infl + 3 * q);
+#pragma unroll
+          for (int n = 0; n < NFD; ++n) rho[n] = fma(sg, D2[q * NFD + n], rho[n]);
+        }
       }
 #pragma unroll
       for (int m = 0; m < NBS; ++m) {

@@ -475,7 +475,13 @@ static int create3d(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdg
   if ((rc = hdgc_dev_alloc(c, (void**)&c->d_minv, NT * sizeof(double)))) return fail(rc);
   if ((rc = hdgc_dev_alloc(c, (void**)&c->d_sign, NT * sizeof(double)))) return fail(rc);
   if ((rc = hdgc_dev_alloc(c, (void**)&c->d_scratch, NT * nb * sizeof(double)))) return fail(rc);
-  if ((rc = hdgc_dev_alloc(c, (void**)&c->d_prep, NT * (4 * (size_t)nqv + 4 * (size_t)nf + 1) * sizeof(double)))) return fail(rc);
+  {
+    // per element: alpha/beta/gamma/delta at the volume points, s at the face points,
+    // the inflow-face mask and the face inflow matrices S_f (Dims3::PREP)
+    const size_t nfd = (size_t)(k + 1) * (k + 2) / 2;
+    const size_t prep = 4 * (size_t)nqv + 4 * (size_t)nf + 1 + 4 * (nfd * (nfd + 1) / 2);
+    if ((rc = hdgc_dev_alloc(c, (void**)&c->d_prep, NT * prep * sizeof(double)))) return fail(rc);
+  }
 #define SETUP3_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) \
     return fail(hdgc_set_err(HDGC_ECUDA, "%s: %s", #x, cudaGetErrorString(e_))); } while (0)
   SETUP3_TRY(cudaMemcpy(c->d_tab, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
