@@ -340,11 +340,20 @@ class ConvectionOperator:
         return wt.cpu().numpy() if host else wt
 
     def substeps_host(self, u: np.ndarray, w: np.ndarray, dt: float, nsteps: int,
-                      inflow: Optional[np.ndarray] = None) -> np.ndarray:
-        """End-to-end substep batch on host arrays (hdgc_substeps_host)."""
+                      inflow: Optional[np.ndarray] = None, inplace: bool = False) -> np.ndarray:
+        """End-to-end substep batch on host arrays (hdgc_substeps_host).
+        ``inplace=True`` updates ``w`` itself (C-contiguous fp64, ideally
+        pinned): no host-side copy, the device reads and writes the caller's
+        buffer directly."""
         lib = _lib.load()
         u = np.ascontiguousarray(u, dtype=np.float64)
-        out = np.array(w, dtype=np.float64, copy=True, order="C")
+        if inplace:
+            if not (isinstance(w, np.ndarray) and w.dtype == np.float64 and w.flags.c_contiguous
+                    and w.flags.writeable):
+                raise ValueError("inplace substeps_host needs a writeable C-contiguous float64 array")
+            out = w
+        else:
+            out = np.array(w, dtype=np.float64, copy=True, order="C")
         ip = None
         if inflow is not None:
             inflow = np.ascontiguousarray(inflow, dtype=np.float64)

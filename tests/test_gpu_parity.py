@@ -107,6 +107,10 @@ def test_host_variants_match_device():
     assert np.array_equal(rd, rh)
     wh = op.substeps_host(g["u"], g["w"], float(g["dt"]), int(g["nsub"]), inflow)
     assert rel(wh, g["w_sub_ld"]) < SUBSTEP_TOL
+    # in place on a pinned host buffer (the bench's e2e path): same bits
+    wp = torch.from_numpy(np.array(g["w"])).pin_memory().numpy()
+    out = op.substeps_host(g["u"], wp, float(g["dt"]), int(g["nsub"]), inflow, inplace=True)
+    assert out is wp and np.array_equal(wp, wh)
 
 
 def test_deterministic_bitwise():
