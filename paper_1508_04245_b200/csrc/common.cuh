@@ -80,4 +80,34 @@ struct ElemParams {
   int nt;
 };
 
+// Programmatic dependent launch (PDL) between consecutive update kernels of a
+// substep batch (hdgc_substeps): kernel s+1 is launched with the
+// programmatic-stream-serialisation attribute, so its CTAs start while kernel
+// s drains its last wave, stage everything that does not depend on w (prep
+// tile, facet tables, neighbour codes, frozen-velocity work) and block in
+// pdl_wait() until kernel s has completed and its writes are visible.  Both
+// instructions are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+// Host side: launch kern<<<grid, block, smem, st>>>(p), with the PDL attribute
+// when pdl is set (the caller guarantees the previous kernel on st is an
+// update kernel of the same batch and nothing before pdl_wait() reads what it
+// writes).
+template <class P>
+inline cudaError_t launch_maybe_pdl(void (*kern)(P), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                                    bool pdl, const P& p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
 }  // namespace hdgc

@@ -60,6 +60,7 @@ struct hdgc_ctx {
   double* d_cres = nullptr;     // (n_curved, nb) raw residual rows (update kernels -> fix-up)
   int64_t bytes = 0;
   int variant = 0;              // 0: thread-per-element (k <= 2), 1: sum-factorised (k >= 3)
+  bool pdl = false;             // next update kernel may launch with PDL (set by hdgc_substeps only)
 };
 
 int hdgc_dev_alloc(hdgc_ctx* c, void** p, size_t bytes);

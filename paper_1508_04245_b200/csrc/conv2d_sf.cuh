@@ -592,8 +592,9 @@ conv2d_sf_kernel(SFParams p) {
                      : "memory");
     }
 #endif
-    bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
     bulk_g2s(s_fD, p.ftab, bt, bar);
+    pdl_wait();   // w is the previous update kernel's output (PDL launch in a substep batch)
+    bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
   }
 
   const int warp = threadIdx.x >> 5;
@@ -613,6 +614,8 @@ conv2d_sf_kernel(SFParams p) {
   if (warp == 0) {
     // ===================== volume warp =====================
     const double mi = (MODE == MODE_SUBSTEP || MODE == MODE_STAGE) && active ? __ldg(p.minv + T) : 0.0;
+    pdl_wait();
+    pdl_trigger();
     mbar_wait(bar, 0);
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
     if (F::RING) sf_rows_ring<K>(wc, gtile, s_prep, active ? le : 0, lane, N - F::FACET_ROWS, r, s_BT);
@@ -652,6 +655,8 @@ conv2d_sf_kernel(SFParams p) {
     int codes[3];
 #pragma unroll
     for (int ed = 0; ed < 3; ++ed) codes[ed] = active ? __ldg(p.code + (size_t)T * 3 + ed) : -1;
+    pdl_wait();   // halo gathers below read the previous kernel's w
+    pdl_trigger();
     mbar_wait(bar, 0);
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
     double* halo = part;

@@ -88,6 +88,10 @@ conv2d_thread_kernel(ElemParams p) {
       dv[i] = a;
     }
   }
+  // everything above depends on u and the tables only; w (and x) are the
+  // previous update kernel's output under a PDL launch (common.cuh)
+  pdl_wait();
+  pdl_trigger();
   double w[NB];
   {
     const double2* wg = reinterpret_cast<const double2*>(p.w + (size_t)T * NB);

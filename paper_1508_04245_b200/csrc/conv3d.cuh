@@ -226,6 +226,8 @@ conv3d_kernel(Conv3Params p) {
     const int f = i / (D::NFD * NBS);
     s_R[f * D::RSTR + (i - f * D::NFD * NBS)] = __ldg(p.rtab + i);
   }
+  pdl_wait();   // w (and x) come from the previous update kernel under PDL (common.cuh)
+  pdl_trigger();
   constexpr bool SR = HDGC_3D_SMEM_R;
   // SR: w_c from smem (s_wo) and the volume accumulators in smem (s_wn doubles as
   // s_r until the face loop), so the sum-factorisation state fits in 136 registers

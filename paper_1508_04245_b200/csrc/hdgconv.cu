@@ -675,7 +675,11 @@ int hdgc_substeps(hdgc_ctx* c, const double* u, double* w, const double* inflow,
     if (rc) return rc;
   }
   for (int s = 0; s < nsteps; ++s) {
+    // substeps after the first overlap their prologue with the previous
+    // substep's drain (PDL, common.cuh); curved batches interpose the fix-up kernel
+    c->pdl = s > 0 && c->n_curved == 0;
     int rc = apply_any(c, MODE_SUBSTEP, u, a, inflow, b, dt, true, st);
+    c->pdl = false;
     if (rc) return rc;
     double* t = a; a = b; b = t;
   }

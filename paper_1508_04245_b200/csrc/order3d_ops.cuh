@@ -75,7 +75,7 @@ int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, d
   constexpr int smem = Dims3<K>::SMEM;
   auto launch = [&](auto kern) -> int {
     if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<blocks, Dims3<K>::THREADS, smem, st>>>(p);
+    CUDA_TRY(launch_maybe_pdl(kern, blocks, Dims3<K>::THREADS, smem, st, c->pdl, p));
     return HDGC_OK;
   };
   int rc = mode == MODE_SUBSTEP ? launch(conv3d_kernel<K, MODE_SUBSTEP>)

@@ -108,8 +108,7 @@ int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w, const d
   const int smem = thread_smem_bytes<K>();
   auto launch = [&](auto kern) -> int {
     if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<blocks, threads, smem, st>>>(p);
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(launch_maybe_pdl(kern, blocks, threads, smem, st, c->pdl, p));
     return HDGC_OK;
   };
   switch (mode) {
@@ -193,8 +192,7 @@ int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double
     const int blocks = (c->nt + F::EPB - 1) / F::EPB;
     auto launch = [&](auto kern) -> int {
       if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      kern<<<blocks, F::THREADS, smem, st>>>(p);
-      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(launch_maybe_pdl(kern, blocks, F::THREADS, smem, st, c->pdl, p));
       return HDGC_OK;
     };
     if (mode == MODE_SUBSTEP) return launch(conv2d_sf_kernel<K, MODE_SUBSTEP>);

@@ -101,3 +101,21 @@ def test_cfg5_shape_substeps_small():
     op.substeps(dev(u), wd, dt, 20, dev(inf))
     ref = O3.substeps3(m, k, u, w, dt, 20, inf)
     assert rel(wd, ref) < SUBSTEP_TOL
+
+
+def test_pdl_batch_bitwise_equals_single_substeps_3d():
+    """3D substep batches use programmatic dependent launch between substeps:
+    bit-identical to one-substep calls (no stale w)."""
+    m = M3.generate_cube(12)
+    k = 3
+    vp = F3.VectorPotential(4, 5)
+    u = F3.interpolate_curl3(m, k, vp)
+    w = F3.transfer_I3_host(m, k, u)
+    op = ConvectionOperator(m, k)
+    ud = dev(u)
+    n, dt = 12, 1e-4
+    batch = op.substeps(ud, dev(w), dt, n)
+    one = dev(w)
+    for _ in range(n):
+        one = op.substeps(ud, one, dt, 1)
+    assert torch.equal(batch, one)

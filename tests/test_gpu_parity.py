@@ -196,3 +196,27 @@ def test_cfg4_order_sweep(k):
     op = ConvectionOperator(m, k)
     r = op.apply(dev(u), dev(w), dev(inf))
     assert rel(r, P.PortOperator(m, k).apply(u, w, inf)) < APPLY_TOL
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 7])
+def test_pdl_batch_bitwise_equals_single_substeps(k):
+    """hdgc_substeps launches substeps 2..n with programmatic dependent launch
+    (the next kernel stages its prep tile while the previous one drains); a
+    missing dependency would read a stale w.  The batch must be bit-identical
+    to n separate one-substep calls (no PDL), on a mesh with many waves."""
+    m = M.generate_structured((0.0, 0.0, 1.0, 1.0), 96, 96)
+    sf = F.StreamFunction(8, 2)
+    u = F.interpolate_curl(m, k, sf)
+    w = F.transfer_I_host(m, k, u)
+    inflow = F.inflow_values(m, k, sf)
+    op = ConvectionOperator(m, k)
+    ud, infd = dev(u), dev(inflow)
+    dt = F.cfl_dt(m.h_min(), k, F.max_speed_host(m, k, u))
+    n = 40
+    batch = op.substeps(ud, dev(w), dt, n, infd)
+    one = dev(w)
+    for _ in range(n):
+        one = op.substeps(ud, one, dt, 1, infd)
+    assert torch.equal(batch, one)
+    for _ in range(3):   # repeated batches: identical (no race on w)
+        assert torch.equal(op.substeps(ud, dev(w), dt, n, infd), batch)
