@@ -80,6 +80,27 @@ struct ElemParams {
   int nt;
 };
 
+// FP64 tensor-core MMA (SASS DMMA), D (8x8) += A (8x4, row) B (4x8, col).
+// Fragments (lane l): a = A[l/4][l%4], b = B[l%4][l/4], d0/d1 = D[l/4][2(l%4) + 0/1].
+__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Host side: A fragments of an (nr x nb) row-major matrix M for dmma_m8n8k4,
+// tile (mt, ks) lane l at [(mt * ks_n + ks) * 32 + l] = M[8 mt + l/4][4 ks + l%4]
+// (zero-padded to 8-row / 4-column multiples).
+inline void dmma_a_fragments(const double* M, int nr, int nb, double* out) {
+  const int mt_n = (nr + 7) / 8, ks_n = (nb + 3) / 4;
+  for (int mt = 0; mt < mt_n; ++mt)
+    for (int ks = 0; ks < ks_n; ++ks)
+      for (int l = 0; l < 32; ++l) {
+        const int i = mt * 8 + l / 4, j = ks * 4 + l % 4;
+        out[(mt * ks_n + ks) * 32 + l] = (i < nr && j < nb) ? M[(size_t)i * nb + j] : 0.0;
+      }
+}
+
 // Programmatic dependent launch (PDL) between consecutive update kernels of a
 // substep batch (hdgc_substeps): kernel s+1 is launched with the
 // programmatic-stream-serialisation attribute, so its CTAs start while kernel

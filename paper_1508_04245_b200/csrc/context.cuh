@@ -34,6 +34,7 @@ struct hdgc_ctx {
   double* d_scratch2 = nullptr; // (NT, nb) r_V for apply_w (lazily allocated)
   double* d_sign = nullptr;     // (NT,) sign(detJ) (3D: sorted-vertex tets)
   double* d_ftab = nullptr;     // facet tables fw | fD (sum-factorised variant)
+  double* d_afrag = nullptr;    // DMMA A fragments of [coef ; divm] (tile prep, k = 3..6)
   // host-variant staging (lazily allocated)
   double* d_hu = nullptr;
   double* d_hw = nullptr;

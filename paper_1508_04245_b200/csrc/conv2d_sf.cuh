@@ -299,6 +299,117 @@ prep_rows2d_kernel(const double* __restrict__ tab, const double* __restrict__ u,
 }
 
 // ---------------------------------------------------------------------------
+// tile prep (k = 3..6): one CTA per 32 elements (two prep tiles), one warp per
+// collapsed row b.
+// Stage 1, the modal rows [u_hat | div u_hat] = M u with M = [coef ; divm]
+// (NR x NB), is a small dense GEMM per CTA: (NR x NB) x (NB x 32 elements), on
+// the FP64 tensor cores (mma.sync m8n8k4 f64, SASS DMMA).  A operands are
+// precomputed host-side in fragment order (PrepMma::afrag, one coalesced
+// 256-B load per fragment, L1-resident across CTAs); B operands come from u
+// staged transposed in smem ([j][e], row stride 40 doubles: the 4 k-rows x 8
+// columns of a fragment load hit 2 wavefronts, the minimum); D fragments go to
+// s_h [i][e] (row stride 40: conflict-free double2 stores).  The LDS-fed DFMA
+// version of this stage was LDS-bandwidth bound (two LDS per FMA).
+// Stage 2: warp b evaluates the velocity on collapsed row b by sum
+// factorisation and writes alpha/beta/gamma of its N points; warps 0..2 also
+// write the inflow weights of edge 0..2.  Table operands are warp-uniform
+// (constant bank); the slot-major prep writes of a warp are two full 128-B
+// segments.
+template <int K>
+struct PrepMma {
+  static constexpr int NB = SF<K>::NB, NR = SF<K>::NB + SF<K>::NBS1;
+  static constexpr int MT = (NR + 7) / 8;      // 8-row tiles of M
+  static constexpr int KS = (NB + 3) / 4;      // k-steps of 4
+  static constexpr int LD = 40;                // smem row stride (doubles) of s_u and s_h
+  static constexpr int AFRAG = MT * KS * 32;   // doubles of precomputed A fragments
+  static constexpr int SMEM = KS * 4 * LD + MT * 8 * LD;   // s_u [KS*4][LD] | s_h [MT*8][LD]
+};
+
+template <int K>
+__global__ void __launch_bounds__(32 * SF<K>::N, 2)
+prep_tile2d_kernel(const double* __restrict__ tab, const double* __restrict__ afrag, const double* __restrict__ u,
+                   int nt, double* __restrict__ prep) {
+  using D = Dims<K>;
+  using F = SF<K>;
+  using P = PrepMma<K>;
+  constexpr int N = F::N, NE = F::NE, NBS = F::NBS, NB = F::NB, NF = F::NF, LD = P::LD;
+  constexpr int NTH = 32 * N;
+  extern __shared__ __align__(16) double smp[];
+  double* s_u = smp;                   // [KS*4][LD]: u transposed, zero rows j >= NB
+  double* s_h = smp + P::KS * 4 * LD;  // [MT*8][LD]: u_hat | div u_hat (rows >= NR unused)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T0 = blockIdx.x * 32;
+  const int nel = min(32, nt - T0);
+  for (int i = tid; i < 32 * NB; i += NTH) {
+    const int e = i / NB, j = i - e * NB;
+    s_u[j * LD + e] = e < nel ? __ldg(u + (size_t)T0 * NB + i) : 0.0;
+  }
+  for (int i = tid; i < (P::KS * 4 - NB) * 32; i += NTH) s_u[(NB + i / 32) * LD + (i & 31)] = 0.0;
+  __syncthreads();
+  // stage 1: (MT x 4) output tiles of 8 x 8 over the warps
+  for (int t = warp; t < P::MT * 4; t += N) {
+    const int mt = t >> 2, n0 = (t & 3) * 8;
+    const double* af = afrag + (size_t)mt * P::KS * 32 + lane;
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < P::KS; ++ks)
+      dmma_m8n8k4(d0, d1, __ldg(af + ks * 32), s_u[(ks * 4 + (lane & 3)) * LD + n0 + (lane >> 2)]);
+    *reinterpret_cast<double2*>(s_h + (mt * 8 + (lane >> 2)) * LD + n0 + 2 * (lane & 3)) = make_double2(d0, d1);
+  }
+  const bool active = lane < nel;
+  double* out = prep + (size_t)(blockIdx.x * 2 + (lane >> 4)) * F::PREP_TILE + (lane & 15);
+  if (warp < 3 && active) {
+    // inflow weights of edge `warp`: F = |e| sum_l u[e(k+1)+l] L_l(t_q)
+    const int ed = warp;
+    const double len = __ldg(tab + D::OFF_FLEN + ed);
+    const double* FL = fl_tab<K>();
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      double a = 0.0;
+#pragma unroll
+      for (int l = 0; l < NE; ++l) a = fma(s_u[(ed * NE + l) * LD + lane], FL[q * NE + l], a);
+      const double Fq = a * len;
+      out[(F::P_S + ed * NF + q) * 16] = Fq < 0.0 ? __ldg(tab + D::OFF_FW + q) * Fq : 0.0;
+    }
+  }
+  __syncthreads();
+  // stage 2: velocity on row b = warp
+  const int b = warp;
+  const double* C = sf_tab<K>();
+  const double* Bb = C + F::C_B + b * NBS;
+  double H0[NE], H1[NE], Hd[NE];
+#pragma unroll
+  for (int i = 0; i <= K; ++i) {
+    double s0 = 0.0, s1 = 0.0, sd = 0.0;
+#pragma unroll
+    for (int j = 0; j <= K - i; ++j) {
+      const int m = midx(i, j);
+      const double bm = Bb[m];
+      s0 = fma(s_h[m * LD + lane], bm, s0);
+      s1 = fma(s_h[(NBS + m) * LD + lane], bm, s1);
+      if (i + j < K) sd = fma(s_h[(NB + m) * LD + lane], bm, sd);
+    }
+    H0[i] = s0; H1[i] = s1; Hd[i] = sd;
+  }
+  if (!active) return;
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+    double u0 = 0.0, u1 = 0.0, dq = 0.0;
+#pragma unroll
+    for (int i = 0; i <= K; ++i) {
+      const double Ai = C[F::C_A + a * NE + i];
+      u0 = fma(Ai, H0[i], u0);
+      u1 = fma(Ai, H1[i], u1);
+      if (i < K) dq = fma(Ai, Hd[i], dq);
+    }
+    const int p = b * N + a;
+    out[(F::P_AL + p) * 16] = fma(C[F::C_PA + p], u0, C[F::C_PB + p] * u1);
+    out[(F::P_BE + p) * 16] = C[F::C_PW + p] * u1;
+    out[(F::P_GA + p) * 16] = C[F::C_PW + p] * dq;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // per-apply / per-substep kernel
 struct SFParams {
   const double* __restrict__ prep;    // tile-blocked [tile][PREP][16]

@@ -191,6 +191,171 @@ prep3d_kernel(Prep3Params p) {
   }
 }
 
+// Tile prep (replaces the thread-per-element prep3d_kernel): one CTA per 32
+// tets, lane = element.
+// Stage 1: modal rows [u_hat | div u_hat] = [coef ; divm] u, (NB + NBS1) x NB
+//   times NB x 32, on the FP64 tensor cores (dmma_m8n8k4, A fragments
+//   precomputed host-side in c->d_afrag; u staged transposed in smem).
+// Faces (warps 0..3 = face f, concurrently with nothing else needing them):
+//   inflow weights s_q at the NF face points, the inflow-face bitmask, and the
+//   face inflow matrix S_f = D2^T diag(s) D2 (upper triangle).
+// Stage 2 (warp = collapsed c-slice ic): the velocity and its divergence at
+//   the n x n points of slice ic by sum factorisation (G_ij(c) -> H_i(b, c) ->
+//   values at (a, b, c)), then the flux-form coefficients alpha..delta with
+//   the Duffy chain rule (C_PF), all tables warp-uniform in the constant bank.
+template <int K>
+struct Prep3Mma {
+  static constexpr int NB = Dims3<K>::NB, NR = Dims3<K>::NB + Dims3<K>::NBS1;
+  static constexpr int MT = (NR + 7) / 8, KS = (NB + 3) / 4;
+  static constexpr int LD = 40;
+  static constexpr int AFRAG = MT * KS * 32;
+  static constexpr int WARPS = SF3<K>::N > 4 ? SF3<K>::N : 4;
+  static constexpr int SMEM = KS * 4 * LD + MT * 8 * LD;   // doubles: s_u | s_h
+};
+
+template <int K>
+__global__ void __launch_bounds__(32 * Prep3Mma<K>::WARPS)
+prep_tile3d_kernel(const double* __restrict__ tab, const double* __restrict__ afrag, const double* __restrict__ u,
+                   const double* __restrict__ sgn, int nt, double* __restrict__ prep) {
+  using D = Dims3<K>;
+  using S = SF3<K>;
+  using P = Prep3Mma<K>;
+  constexpr int NB = D::NB, NBS = D::NBS, NFD = D::NFD, NQ = D::NQ, NF = D::NF, LD = P::LD;
+  constexpr int N = S::N, NE = S::NE, NPAIR = S::NPAIR, NTH = 32 * P::WARPS;
+  extern __shared__ __align__(16) double smq[];
+  double* s_u = smq;                    // [KS*4][LD]
+  double* s_h = smq + P::KS * 4 * LD;   // [MT*8][LD]
+  __shared__ unsigned s_mask[32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T0 = blockIdx.x * 32;
+  const int nel = min(32, nt - T0);
+  for (int i = tid; i < 32 * NB; i += NTH) {
+    const int e = i / NB, j = i - e * NB;
+    s_u[j * LD + e] = e < nel ? __ldg(u + (size_t)T0 * NB + i) : 0.0;
+  }
+  for (int i = tid; i < (P::KS * 4 - NB) * 32; i += NTH) s_u[(NB + i / 32) * LD + (i & 31)] = 0.0;
+  if (tid < 32) s_mask[tid] = 0u;
+  __syncthreads();
+  for (int t = warp; t < P::MT * 4; t += P::WARPS) {
+    const int mt = t >> 2, n0 = (t & 3) * 8;
+    const double* af = afrag + (size_t)mt * P::KS * 32 + lane;
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll 5
+    for (int ks = 0; ks < P::KS; ++ks)
+      dmma_m8n8k4(d0, d1, __ldg(af + ks * 32), s_u[(ks * 4 + (lane & 3)) * LD + n0 + (lane >> 2)]);
+    *reinterpret_cast<double2*>(s_h + (mt * 8 + (lane >> 2)) * LD + n0 + 2 * (lane & 3)) = make_double2(d0, d1);
+  }
+  const bool active = lane < nel;
+  const int T = T0 + (active ? lane : 0);
+  const double sg = __ldg(sgn + T);
+  const size_t nts = (size_t)nt;
+  if (warp < 4) {
+    // ---- face f = warp: inflow weights, bitmask, inflow matrix
+    const int f = warp;
+    const double len = __ldg(tab + D::OFF_FLEN + f);
+    const double* D2 = c_sf3d + S::C_D2;
+    double sv[NF];
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      double a = 0.0;
+#pragma unroll
+      for (int m = 0; m < NFD; ++m) a = fma(s_u[(f * NFD + m) * LD + lane], __ldg(tab + D::OFF_FL + q * NFD + m), a);
+      const double F = sg * a * len;
+      sv[q] = F < 0.0 ? __ldg(tab + D::OFF_FW + q) * F : 0.0;
+      any |= F < 0.0;
+    }
+    // the substep kernel reads s and S_f of a face only when its inflow bit is
+    // set, so outflow faces write nothing
+    if (any && active) {
+      atomicOr(&s_mask[lane], 1u << f);
+#pragma unroll
+      for (int q = 0; q < NF; ++q) prep[(size_t)(4 * NQ + f * NF + q) * nts + T] = sv[q];
+      // fully unrolled: every D2 entry is an immediate constant-bank operand (a
+      // runtime-indexed version spent 58% of the kernel in LDC/MIO stalls); k=4
+      // (120 x 49 terms) would spill, so it keeps runtime n, n2
+      auto sf_entry = [&](int n, int n2) {
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q < NF; ++q) a = fma(sv[q] * D2[q * NFD + n], D2[q * NFD + n2], a);
+        prep[(size_t)(D::P_S + f * D::NSYM + n * NFD - n * (n - 1) / 2 + (n2 - n)) * nts + T] = a;
+      };
+      if constexpr (K <= 3) {
+#pragma unroll
+        for (int n = 0; n < NFD; ++n)
+#pragma unroll
+          for (int n2 = n; n2 < NFD; ++n2) sf_entry(n, n2);
+      } else {
+#pragma unroll 1
+        for (int n = 0; n < NFD; ++n)
+#pragma unroll 1
+          for (int n2 = n; n2 < NFD; ++n2) sf_entry(n, n2);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0 && active) prep[(size_t)D::P_MASK * nts + T] = (double)s_mask[lane];
+  if (warp >= N) return;
+  // ---- stage 2: collapsed slice ic = warp
+  const int ic = warp;
+  const double* Cs = c_sf3d;
+  const double* Cc = Cs + S::C_C + ic * NBS;
+  double G0[NPAIR], G1[NPAIR], G2[NPAIR], Gd[NPAIR];
+#pragma unroll
+  for (int i = 0; i <= K; ++i)
+#pragma unroll
+    for (int j = 0; j <= K - i; ++j) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, sd = 0.0;
+#pragma unroll
+      for (int l = 0; l <= K - i - j; ++l) {
+        const int m = midx3(i, j, l);
+        const double cm = Cc[m];
+        s0 = fma(s_h[m * LD + lane], cm, s0);
+        s1 = fma(s_h[(NBS + m) * LD + lane], cm, s1);
+        s2 = fma(s_h[(2 * NBS + m) * LD + lane], cm, s2);
+        if (i + j + l < K) sd = fma(s_h[(NB + m) * LD + lane], cm, sd);
+      }
+      G0[pidx(i, j)] = s0; G1[pidx(i, j)] = s1; G2[pidx(i, j)] = s2; Gd[pidx(i, j)] = sd;
+    }
+  if (!active) return;
+#pragma unroll 1
+  for (int ib = 0; ib < N; ++ib) {
+    const double* Bb = Cs + S::C_B + ib * NPAIR;
+    double H0[NE], H1[NE], H2[NE], Hd[NE];
+#pragma unroll
+    for (int i = 0; i <= K; ++i) {
+      double h0 = 0.0, h1 = 0.0, h2 = 0.0, hd = 0.0;
+#pragma unroll
+      for (int j = 0; j <= K - i; ++j) {
+        const double bb = Bb[pidx(i, j)];
+        h0 = fma(G0[pidx(i, j)], bb, h0);
+        h1 = fma(G1[pidx(i, j)], bb, h1);
+        h2 = fma(G2[pidx(i, j)], bb, h2);
+        if (i + j < K) hd = fma(Gd[pidx(i, j)], bb, hd);
+      }
+      H0[i] = h0; H1[i] = h1; H2[i] = h2; Hd[i] = hd;
+    }
+#pragma unroll
+    for (int ia = 0; ia < N; ++ia) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, dq = 0.0;
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        const double Ai = Cs[S::C_A + ia * NE + i];
+        a0 = fma(Ai, H0[i], a0);
+        a1 = fma(Ai, H1[i], a1);
+        a2 = fma(Ai, H2[i], a2);
+        if (i < K) dq = fma(Ai, Hd[i], dq);
+      }
+      const int q = (ic * N + ib) * N + ia;
+      const double* pf = Cs + S::C_PF + q * 5;
+      prep[(size_t)q * nts + T] = sg * fma(pf[0], a0, pf[1] * (a1 + a2));
+      prep[(size_t)(NQ + q) * nts + T] = sg * fma(pf[2], a1, pf[3] * a2);
+      prep[(size_t)(2 * NQ + q) * nts + T] = sg * pf[4] * a2;
+      prep[(size_t)(3 * NQ + q) * nts + T] = sg * pf[4] * dq;
+    }
+  }
+}
+
 struct Conv3Params {
   const double* __restrict__ tab;
   const double* __restrict__ rtab;    // face trace maps R[4][NFD][NBS]

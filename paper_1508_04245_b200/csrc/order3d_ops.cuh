@@ -1,5 +1,6 @@
 // order3d_ops.cuh — per-order launchers of the 3D kernels (included by order3d_k<K>.cu).
 #pragma once
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -40,6 +41,16 @@ int launch3_setup(hdgc_ctx* c, const hdgc_tables_desc* t) {
       }
   int rc = hdgc_dev_alloc(c, (void**)&c->d_ftab, sizeof(double) * R.size());
   if (rc) return rc;
+  {
+    // A fragments of prep_tile3d_kernel's DMMA stage: M = [coef ; divm] ((NB + NBS1) x NB)
+    using P = Prep3Mma<K>;
+    std::vector<double> M((size_t)P::NR * P::NB), af(P::AFRAG);
+    memcpy(M.data(), t->coef, sizeof(double) * P::NB * P::NB);
+    memcpy(M.data() + (size_t)P::NB * P::NB, t->div_modal, sizeof(double) * (P::NR - P::NB) * P::NB);
+    dmma_a_fragments(M.data(), P::NR, P::NB, af.data());
+    if ((rc = hdgc_dev_alloc(c, (void**)&c->d_afrag, sizeof(double) * af.size()))) return rc;
+    CUDA_TRY(cudaMemcpy(c->d_afrag, af.data(), sizeof(double) * af.size(), cudaMemcpyHostToDevice));
+  }
   CUDA_TRY(cudaMemcpy(c->d_ftab, R.data(), sizeof(double) * R.size(), cudaMemcpyHostToDevice));
   return HDGC_OK;
 }
@@ -52,7 +63,21 @@ int launch3_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
   p.sgn = c->d_sign;
   p.prep = c->d_prep;
   p.nt = c->nt;
-  prep3d_kernel<K><<<grid3_for(c->nt, 128), 128, 0, st>>>(p);
+  static const bool tile = [] {
+    const char* e = getenv("HDGC_PREP");
+    return !(e && e[0] == '0');
+  }();
+  if (tile) {
+    // measured at cfg5 (196608 tets, k=3): see DESIGN.md §10
+    using P = Prep3Mma<K>;
+    const int smem = P::SMEM * (int)sizeof(double);
+    if (smem > 48 * 1024)
+      CUDA_TRY(cudaFuncSetAttribute(prep_tile3d_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    prep_tile3d_kernel<K><<<grid3_for(c->nt, 32), 32 * P::WARPS, smem, st>>>(c->d_tab, c->d_afrag, u, c->d_sign,
+                                                                            c->nt, c->d_prep);
+  } else {
+    prep3d_kernel<K><<<grid3_for(c->nt, 128), 128, 0, st>>>(p);
+  }
   CUDA_TRY(cudaGetLastError());
   return HDGC_OK;
 }

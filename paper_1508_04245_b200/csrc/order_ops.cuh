@@ -1,5 +1,6 @@
 // order_ops.cuh — per-order kernel launchers (included by order_k<K>.cu only).
 #pragma once
+#include <cstdlib>
 #include <cstring>
 
 #include "context.cuh"
@@ -151,10 +152,26 @@ int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st) 
 // frozen-velocity prep rows (alpha | beta | gamma | s) into c->d_prep
 template <int K>
 int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
-  // k <= 4: one fused thread-per-element kernel (matrices in the constant
-  // bank) beats DGEMM + rows (k=3: 35 vs 56 us, k=4: 71 vs 91 us at 131072
-  // elements); from k = 5 the DGEMM path wins (k=5 128 vs 305 us, k=8 340 us
-  // vs 3.4 ms for the old thread-per-point stage 2).
+  // Measured per launch at 131072 elements (ncu, cold): k=3 the fused
+  // thread-per-element kernel (24 us; tile 39 us); k=4..6 the tile kernel with
+  // its DMMA modal stage (k=4 66 us vs fused 84; k=5 124 vs DGEMM 41 + rows 78;
+  // k=6 172 vs 81 + 125); k=7,8: DGEMM + rows (the modal matrix outgrows the
+  // tile kernel's fragment set).  HDGC_PREP=0 selects the older paths (A/B).
+  if constexpr (K >= 4 && K <= 6) {
+    static const bool tile = [] {
+      const char* e = getenv("HDGC_PREP");
+      return !(e && e[0] == '0');
+    }();
+    if (tile && c->d_afrag) {
+      const int smem = PrepMma<K>::SMEM * (int)sizeof(double);
+      if (smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(prep_tile2d_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      prep_tile2d_kernel<K><<<(c->nt + 31) / 32, 32 * SF<K>::N, smem, st>>>(c->d_tab, c->d_afrag, u, c->nt,
+                                                                          c->d_prep);
+      CUDA_TRY(cudaGetLastError());
+      return HDGC_OK;
+    }
+  }
   if constexpr (K >= 3 && K <= 4) {
     prep_fused2d_kernel<K><<<grid_for(c->nt, 128), 128, 0, st>>>(u, c->nt, c->d_prep);
     CUDA_TRY(cudaGetLastError());
@@ -252,6 +269,15 @@ int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& 
       CUDA_TRY(cudaMemcpyToSymbol(c_cm, cm.data(), sizeof(double) * cm.size()));
     }
 #endif
+    if constexpr (K >= 4 && K <= 6) {
+      // A fragments of the tile prep's DMMA stage (prep_tile2d_kernel): M = [coef ; divm]
+      using P = PrepMma<K>;
+      std::vector<double> af(P::AFRAG, 0.0);
+      dmma_a_fragments(&packed[D::OFF_COEF], P::NR, P::NB, af.data());   // coef rows then divm rows
+      int rc0 = hdgc_dev_alloc(c, (void**)&c->d_afrag, sizeof(double) * P::AFRAG);
+      if (rc0) return rc0;
+      CUDA_TRY(cudaMemcpy(c->d_afrag, af.data(), sizeof(double) * P::AFRAG, cudaMemcpyHostToDevice));
+    }
     int rc = hdgc_dev_alloc(c, (void**)&c->d_ftab, sizeof(double) * F::TAB_PAD);
     if (rc) return rc;
     CUDA_TRY(cudaMemcpy(c->d_ftab, ft.data(), sizeof(double) * F::TAB_PAD, cudaMemcpyHostToDevice));
