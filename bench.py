@@ -254,6 +254,7 @@ def main():
     for i in range(args.steps):
         wd.copy_(w0)
         flush.fill_(float(i))
+        torch.cuda._sleep(200000)   # ~0.1 ms spin: the host enqueue of the step overlaps it, not the timed region
         ev[i][0].record(stream)
         step()
         ev[i][1].record(stream)

@@ -1,8 +1,9 @@
 """Throughput of every BASELINE.json config on one B200 (development / report
 tool; bench.py is the driver contract and measures cfg2 only).
 
-One JSON line per (config, k): the single-apply time (prep + kernel, median of
-`--reps` calls, L2 flushed by a 512 MB write before each), the substep-batch
+One JSON line per (config, k): the single-apply device time (prep + kernel,
+median of `reps` calls, L2 flushed by a 512 MB write before each, host enqueue
+hidden behind a spin kernel), the substep-batch
 time of the config's substep count (whole batch incl. its one prep, divided
 by n, L2 flushed before the batch), DOF/s and applies/s for both, and the
 pinned-roofline fraction (F(k) flop and B(k) bytes per element;
@@ -40,9 +41,15 @@ def pinned3(k):
 
 
 def timed(fn, reps, flush):
+    """Device time of fn() (median over reps, L2 flushed before each).  A
+    ~100 us spin kernel is queued before the start event, so the host-side
+    enqueue cost of fn (Python + ctypes, ~10-20 us) overlaps it instead of
+    showing up as device idle time inside the timed region (it dominated the
+    small cfg1 / cfg4 applies)."""
     ts = []
     for _ in range(reps):
         flush.fill_(1.0)
+        torch.cuda._sleep(200000)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         fn()
@@ -83,6 +90,7 @@ def report(cfg, m, k, u, w, inf, nsub, dim, reps, flush, dt):
         for _ in range(max(3, reps // 4)):
             wd.copy_(w0)
             flush.fill_(1.0)
+            torch.cuda._sleep(200000)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             op.substeps(ud, wd, dt, nsub, infd)
