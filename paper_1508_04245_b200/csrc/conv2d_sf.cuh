@@ -240,7 +240,21 @@ prep_rows2d_kernel(const double* __restrict__ tab, const double* __restrict__ u,
   __shared__ double s_mod[16 * NR];
   const int T0 = blockIdx.x * 16;
   const int nel = min(16, nt - T0);
-  for (int i = threadIdx.x; i < nel * NR; i += blockDim.x) s_mod[i] = __ldg(modal + (size_t)T0 * NR + i);
+  {
+    // every load of this thread in flight before the smem stores
+    constexpr int LOADS = (16 * NR + 16 * N - 1) / (16 * N);
+    double v[LOADS];
+#pragma unroll
+    for (int r = 0; r < LOADS; ++r) {
+      const int i = threadIdx.x + r * 16 * N;
+      v[r] = i < nel * NR ? __ldg(modal + (size_t)T0 * NR + i) : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < LOADS; ++r) {
+      const int i = threadIdx.x + r * 16 * N;
+      if (i < nel * NR) s_mod[i] = v[r];
+    }
+  }
   __syncthreads();
   const int e = threadIdx.x & 15;
   const int b = threadIdx.x >> 4;

@@ -399,9 +399,21 @@ conv3d_kernel(Conv3Params p) {
   double* s_R = sm3;                     // [4][NFD][NBS]
   double* s_wo = sm3 + D::RTAB;          // [NBS][96]
   double* s_wn = s_wo + NBS * 96;        // [NBS][96]
-  for (int i = threadIdx.x; i < 4 * D::NFD * NBS; i += blockDim.x) {
-    const int f = i / (D::NFD * NBS);
-    s_R[f * D::RSTR + (i - f * D::NFD * NBS)] = __ldg(p.rtab + i);
+  {
+    // trace maps: every load of this thread in flight before the smem stores
+    constexpr int TOT = 4 * D::NFD * NBS, LOADS = (TOT + D::THREADS - 1) / D::THREADS;
+    double v[LOADS];
+#pragma unroll
+    for (int r = 0; r < LOADS; ++r) {
+      const int i = threadIdx.x + r * D::THREADS;
+      v[r] = i < TOT ? __ldg(p.rtab + i) : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < LOADS; ++r) {
+      const int i = threadIdx.x + r * D::THREADS;
+      const int f = i / (D::NFD * NBS);
+      if (i < TOT) s_R[f * D::RSTR + (i - f * D::NFD * NBS)] = v[r];
+    }
   }
   pdl_wait();   // w (and x) come from the previous update kernel under PDL (common.cuh)
   pdl_trigger();
