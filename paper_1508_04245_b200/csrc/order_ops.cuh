@@ -153,11 +153,11 @@ int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st) 
 template <int K>
 int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
   // Measured per launch at 131072 elements (ncu, cold): k=3 the fused
-  // thread-per-element kernel (24 us; tile 39 us); k=4..6 the tile kernel with
+  // thread-per-element kernel (24 us; tile 39 us); k>=4 the tile kernel with
   // its DMMA modal stage (k=4 54 us vs fused 84; k=5 98 vs DGEMM 41 + rows 78;
-  // k=6 136 vs 81 + 125); k=7,8: DGEMM + rows (the modal matrix outgrows the
-  // tile kernel's fragment set).  HDGC_PREP=0 selects the older paths (A/B).
-  if constexpr (K >= 4 && K <= 6) {
+  // k=6 136 vs 81 + 125; k=7 241 vs 102 + 220; k=8 386 vs 123 + 293).
+  // HDGC_PREP=0 selects the older paths (A/B).
+  if constexpr (K >= 4) {
     static const bool tile = [] {
       const char* e = getenv("HDGC_PREP");
       return !(e && e[0] == '0');
@@ -269,7 +269,7 @@ int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& 
       CUDA_TRY(cudaMemcpyToSymbol(c_cm, cm.data(), sizeof(double) * cm.size()));
     }
 #endif
-    if constexpr (K >= 4 && K <= 6) {
+    if constexpr (K >= 4) {
       // A fragments of the tile prep's DMMA stage (prep_tile2d_kernel): M = [coef ; divm]
       using P = PrepMma<K>;
       std::vector<double> af(P::AFRAG, 0.0);
