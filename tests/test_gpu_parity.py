@@ -220,3 +220,42 @@ def test_pdl_batch_bitwise_equals_single_substeps(k):
     assert torch.equal(batch, one)
     for _ in range(3):   # repeated batches: identical (no race on w)
         assert torch.equal(op.substeps(ud, dev(w), dt, n, infd), batch)
+
+
+_AB_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from conftest import load_golden
+from paper_1508_04245_b200 import mesh as M, mesh3d as M3
+from paper_1508_04245_b200.forms import ConvectionOperator
+dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+out = []
+for name in ("sweep_k4", "sweep_k5", "jit_k6", "sweep_k8"):
+    g = load_golden(f"conv_{name}.npz")
+    m = M.build_mesh(g["vertices"], g["triangles"])
+    inf = dev(g["inflow"]) if "inflow" in g.files else None
+    op = ConvectionOperator(m, int(g["k"]))
+    r = op.apply(dev(g["u"]), dev(g["w_rand"]), inf).cpu().numpy()
+    out.append(np.linalg.norm(r - g["r_rand_ld"]) / np.linalg.norm(g["r_rand_ld"]))
+g = load_golden("conv3d_k3.npz")
+op = ConvectionOperator(M3.generate_cube(int(g["n"])), 3)
+r = op.apply(dev(g["u"]), dev(g["w_rand"]), dev(g["inflow"])).cpu().numpy()
+out.append(np.linalg.norm(r - g["r_rand_ld"]) / np.linalg.norm(g["r_rand_ld"]))
+print(" ".join(f"{x:.3e}" for x in out))
+"""
+
+
+def test_prep_fallback_paths_hdgc_prep_0():
+    """HDGC_PREP=0 keeps the pre-tile prep paths (fused thread-per-element,
+    DGEMM + rows, thread-per-element 3D) for A/B timing; they must stay at
+    parity too (the default tile path is covered by the golden tests)."""
+    import os
+    import subprocess
+    import sys
+    tests = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, HDGC_PREP="0")
+    res = subprocess.run([sys.executable, "-c", _AB_SCRIPT, tests], env=env, capture_output=True, text=True,
+                         timeout=600, cwd=os.path.dirname(tests))
+    assert res.returncode == 0, res.stderr[-2000:]
+    errs = [float(x) for x in res.stdout.split()]
+    assert len(errs) == 5 and max(errs) < APPLY_TOL, errs
