@@ -38,7 +38,7 @@ __host__ __device__ constexpr int thread_smem_bytes() { return 3 * Dims<K>::NF *
 constexpr int THREAD_BLOCK = 64;   // small blocks: 2048 CTAs at 131k elements fill the SMs in ~2 full waves
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(THREAD_BLOCK)
+__global__ void __launch_bounds__(THREAD_BLOCK, K == 2 ? 8 : 14)   // 128 / 72 registers: 8 / 14 CTAs per SM
 conv2d_thread_kernel(ElemParams p) {
   static_assert(K == HDGC_ORDER && K <= 2, "thread variant: k <= 2, tables per translation unit");
   using D = Dims<K>;
@@ -55,11 +55,13 @@ conv2d_thread_kernel(ElemParams p) {
   // neighbour-side facet traces are indexed by the neighbour's local edge (per
   // lane): from a shared-memory copy instead of divergent constant loads
   extern __shared__ __align__(16) double s_fD[];
+  // (filled here, first read in the facet loop: the barrier sits there, so the
+  // table's global latency overlaps the u loads and the volume term)
   for (int i = threadIdx.x; i < 3 * NF * NBS; i += blockDim.x) s_fD[i] = p.tab[D::OFF_FD + i];
-  __syncthreads();
 
-  const int T = blockIdx.x * blockDim.x + threadIdx.x;
-  if (T >= p.nt) return;
+  const int T0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = T0 < p.nt;
+  const int T = active ? T0 : p.nt - 1;   // tail lanes recompute the last element, write nothing
 
   // modal velocity u_hat = coef u and its modal divergence dv = divm u (in P_{k-1})
   double uh[NB];
@@ -136,6 +138,7 @@ conv2d_thread_kernel(ElemParams p) {
     }
   }
 
+  __syncthreads();   // s_fD complete
   // ---- facets: upwind jump on inflow points only (element-owned, no atomics)
 #pragma unroll
   for (int e = 0; e < 3; ++e) {
@@ -203,6 +206,7 @@ conv2d_thread_kernel(ElemParams p) {
   }
 
   // ---- epilogue
+  if (!active) return;
   double* og = p.out + (size_t)T * NB;
   if ((MODE == MODE_SUBSTEP || MODE == MODE_STAGE) && p.st.cres) {
     const double mflag = __ldg(p.minv + T);
