@@ -340,7 +340,7 @@ struct PrepMma {
 };
 
 template <int K>
-__global__ void __launch_bounds__(32 * SF<K>::N, 2)
+__global__ void __launch_bounds__(32 * SF<K>::N, K == 4 ? 4 : (K <= 6 ? 3 : 2))
 prep_tile2d_kernel(const double* __restrict__ tab, const double* __restrict__ afrag, const double* __restrict__ u,
                    int nt, double* __restrict__ prep) {
   using D = Dims<K>;
