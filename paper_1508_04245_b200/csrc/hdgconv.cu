@@ -703,15 +703,17 @@ int hdgc_propagate(hdgc_ctx* c, const double* u_prev, const double* u_cur, doubl
     return rc;
   // velocity at pseudo time s; the prep (variants 1/2) is redone only when s changes
   bool have = false;
+  bool after_update = false;   // last launch on st was an update kernel: the next may use PDL
   double at = 0.0;
   auto velocity = [&](double s, const double** uu) -> int {
     if (!u_prev) {
       *uu = u_cur;
-      if (!have) { have = true; return prep_any(c, u_cur, st); }
+      if (!have) { have = true; after_update = false; return prep_any(c, u_cur, st); }
       return HDGC_OK;
     }
     *uu = c->d_uext;
     if (have && s == at) return HDGC_OK;
+    after_update = false;
     const double th = (s - t_cur) / (t_cur - t_prev);
     axpby_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(u_cur, u_prev, 1.0 + th, -th, c->d_uext, n);
     CUDA_TRY(cudaGetLastError());
@@ -730,13 +732,22 @@ int hdgc_propagate(hdgc_ctx* c, const double* u_prev, const double* u_cur, doubl
     double* v1 = bufs[(cur + 1) % nbuf];
     StageParams sp;
     sp.c = -ds;
-    if ((rc = apply_any(c, MODE_SUBSTEP, uu, v, inflow, v1, sp, true, st))) return rc;
+    // PDL between back-to-back update kernels (common.cuh); not after a prep / axpby
+    c->pdl = after_update && c->n_curved == 0;
+    rc = apply_any(c, MODE_SUBSTEP, uu, v, inflow, v1, sp, true, st);
+    c->pdl = false;
+    if (rc) return rc;
+    after_update = true;
     if (scheme == 0) { cur = (cur + 1) % nbuf; continue; }
     if ((rc = velocity(s1, &uu))) return rc;
     double* v2 = bufs[(cur + 2) % 3];
     StageParams s2;
     s2.a = 0.5; s2.b = 0.5; s2.c = -0.5 * ds; s2.x = v;
-    if ((rc = apply_any(c, MODE_STAGE, uu, v1, inflow, v2, s2, true, st))) return rc;
+    c->pdl = after_update && c->n_curved == 0;
+    rc = apply_any(c, MODE_STAGE, uu, v1, inflow, v2, s2, true, st);
+    c->pdl = false;
+    if (rc) return rc;
+    after_update = true;
     cur = (cur + 2) % 3;
   }
   if (bufs[cur] != w) CUDA_TRY(cudaMemcpyAsync(w, bufs[cur], sizeof(double) * n, cudaMemcpyDeviceToDevice, st));

@@ -70,6 +70,25 @@ def test_propagate_euler_frozen_equals_substeps(k):
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("k", [2, 4])
+def test_propagate_ssprk2_batch_bitwise_equals_single_steps(k):
+    """Consecutive update kernels of a propagate batch launch with PDL; a
+    batch must be bit-identical to one-step calls (no stale v / x reads), on a
+    mesh with many CTA waves."""
+    m = M.generate_structured((0, 0, 1, 1), 96, 96)
+    sf = F.StreamFunction(6, 3, wind=(1.0, 0.3))
+    u = F.interpolate_curl(m, k, sf)
+    w = F.transfer_I_host(m, k, u)
+    inflow = dev(F.inflow_values(m, k, sf))
+    op = ConvectionOperator(m, k)
+    dt = 0.5 * TL.cfl_substep(F.max_speed_host(m, k, u), m.h_min(), k)
+    ud, a, b = dev(u), dev(w), dev(w)
+    op.propagate(ud, a, dt, 20, inflow, "ssprk2")
+    for _ in range(20):
+        op.propagate(ud, b, dt, 1, inflow, "ssprk2")
+    assert torch.equal(a, b)
+
+
 def test_propagate_convection_api_extrapolated():
     k = 3
     m, u, u_prev, w, inflow, apply, minv, _ = case2d(k)
