@@ -155,8 +155,44 @@ def ncu_fp64_flop(nc: dict):
         return None
 
 
+def bench_config(m, dt, world):
+    """The `config` object of both arms (identical, so the driver can match them)."""
+    nb = (K_ORDER + 1) * (K_ORDER + 2)
+    return {"workload": "cfg2: unit square 256x256 -> 131072 affine triangles, BDM_4/V_h k=4, "
+                        "seeded div-free stream function (modes<=16), 100 forward-Euler substeps per step",
+            "elements": m.n_elements, "k": K_ORDER, "dofs_per_apply": m.n_elements * nb, "substeps_per_step": NSUB,
+            "dt": dt, "l2": "flushed (512 MB write) before every timed step",
+            "parallelism": f"replicas x{world}"}
+
+
+def numpy_oracle_sample(n_cells=64):
+    """Single-thread numpy oracle (oracle/convection.py textbook form, fp64;
+    BASELINE.md §2 asks for it beside the multi-core baseline) on a bounded
+    sample: cfg2's field and order on an n x n sub-mesh, one apply."""
+    from threadpoolctl import threadpool_limits
+    from oracle import convection as O
+    from paper_1508_04245_b200 import fields as F
+    from paper_1508_04245_b200 import mesh as M
+    m = M.generate_structured((0.0, 0.0, 1.0, 1.0), n_cells, n_cells)
+    sf = F.StreamFunction(MODES, SEED)
+    u = F.interpolate_curl(m, K_ORDER, sf)
+    w = F.transfer_I_host(m, K_ORDER, u)
+    inflow = F.inflow_values(m, K_ORDER, sf)
+    nb = (K_ORDER + 1) * (K_ORDER + 2)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        O.apply_convection(m, K_ORDER, u, w, inflow)
+        t = time.perf_counter() - t0
+    return {"value": m.n_elements * nb / t, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"one apply of oracle/convection.py (numpy, 1 thread) on {n_cells}x{n_cells} "
+                      f"({m.n_elements} triangles), k={K_ORDER}, cfg2's field: {t:.2f} s"}
+
+
 def run_reference(args, world, rank):
-    """CPU arm: the oracle's OpenMP C port on all host cores (rank 0 only)."""
+    """Reference arm: the reference ships no implementation of this operator
+    (SURVEY §0), so it is the oracle's OpenMP C port (oracle/conv_port.c,
+    "kind": "port") on all host cores, rank 0 only, running the SAME step as
+    the GPU arm: 100 forward-Euler substeps of cfg2 per step."""
     if rank != 0:
         return
     from oracle import port as P
@@ -165,25 +201,25 @@ def run_reference(args, world, rank):
     threads = os.cpu_count() or 1
     op = P.PortOperator(m, K_ORDER, threads=threads)
     nb = (K_ORDER + 1) * (K_ORDER + 2)
-    nsub = 1      # bounded sample: one substep over the full cfg2 mesh per step
-    for _ in range(args.warmup):
-        op.substeps(u, w, dt, nsub, inflow)
+    steps, warm = max(1, args.steps), max(1, min(args.warmup, 3))
+    for _ in range(warm):
+        op.substeps(u, w, dt, NSUB, inflow)
     times = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         t0 = time.perf_counter()
-        op.substeps(u, w, dt, nsub, inflow)
+        op.substeps(u, w, dt, NSUB, inflow)
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
-    value = m.n_elements * nb * nsub / t
+    value = m.n_elements * nb * NSUB / t
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "steps": steps, "warmup": warm, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg2: 256x256 structured, 131072 triangles, k=4, 1 forward-Euler substep per step "
-                               "(bounded CPU sample of the 100-substep GPU step)",
-                   "elements": m.n_elements, "k": K_ORDER, "substeps_per_step": nsub},
+        "config": bench_config(m, dt, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{nsub} substep(s) of cfg2 per step, {args.steps} steps"},
+                         "sample": f"{NSUB} forward-Euler substeps of cfg2 per step (the GPU arm's step), "
+                                   f"{steps} timed steps after {warm} warm-up, oracle/conv_port.c OpenMP"},
+        "numpy_oracle_1thread": numpy_oracle_sample(),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -305,16 +341,13 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = cpu_baseline_sample(m, u, w, inflow, dt)
+        cpu["numpy_oracle_1thread"] = numpy_oracle_sample()
     hbm, hbm_src = hbm_peak()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg2: unit square 256x256 -> 131072 affine triangles, BDM_4/V_h k=4, "
-                               "seeded div-free stream function (modes<=16), 100 forward-Euler substeps per step",
-                   "elements": NT, "k": K_ORDER, "dofs_per_apply": NT * nb, "substeps_per_step": NSUB,
-                   "dt": dt, "l2": "flushed (512 MB write) before every timed step",
-                   "parallelism": f"replicas x{world}"},
+        "config": bench_config(m, dt, world),
         "applies_per_s": world * NSUB / t_step,
         "kernel_us_per_substep": k_s * 1e6,
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

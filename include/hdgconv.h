@@ -21,7 +21,9 @@
  *  - all fp64, row-major, contiguous.
  *
  * Memory: every double* argument of the compute calls is a DEVICE pointer
- * owned by the caller (no allocation in hot calls), except the *_host
+ * owned by the caller, 16-byte aligned (rows move with 16-byte vector loads
+ * and TMA bulk copies; misaligned pointers are rejected with HDGC_EINVAL), no
+ * allocation in hot calls, except the *_host
  * variants, which take pageable or pinned HOST pointers and stage through
  * context-owned device buffers.  `stream` is a cudaStream_t (NULL = legacy
  * default stream); all calls are asynchronous on it except the *_host ones,
@@ -49,6 +51,7 @@ extern "C" {
 #define HDGC_ENOMEM (-3)   /* device allocation failed */
 #define HDGC_EUNSUP (-4)   /* unsupported order / dimension */
 #define HDGC_ENOCONV (-5)  /* Richardson iteration hit max_iter (result = last iterate) */
+#define HDGC_EBLOWUP (-6)  /* norm blow-up: an explicit update produced non-finite values */
 
 typedef struct hdgc_ctx hdgc_ctx;
 
@@ -64,7 +67,11 @@ typedef struct {
   const int64_t* elements;   /* (NT, dim+1) vertex ids */
   const int64_t* facet_elems;/* (NF, 2) */
   const int64_t* facet_local;/* (NF, 2) */
-  const int32_t* facet_perm; /* 3D only: (NF,) neighbour face permutation id; NULL in 2D */
+  const int32_t* facet_perm; /* reserved, must be NULL.  3D meshes must list every tet's vertex
+                              * ids in ascending order (mesh3d.py does): a shared face then has the
+                              * same vertex order, hence the same face parametrisation, on both
+                              * sides, and no face permutation is needed.  Unsorted tets are
+                              * rejected with HDGC_EINVAL. */
 } hdgc_mesh_desc;
 
 /* Reference-element tables, HOST arrays (copied at create), produced by the
@@ -109,7 +116,11 @@ typedef struct {
 } hdgc_info;
 
 /* Build a context: uploads tables, runs the on-device geometry/adjacency
- * precompute (Piola factors J/detJ, 2/detJ, neighbour codes, boundary slots). */
+ * precompute (Piola factors J/detJ, 2/detJ, neighbour codes, boundary slots).
+ * The mesh is validated on the device: vertex ids in range, element ids and
+ * local facet ids in range, every (element, local facet) in exactly one facet,
+ * positive detJ (2D) / nonzero detJ and ascending vertex ids (3D); failures
+ * return HDGC_EINVAL with the reason in hdgc_last_error(). */
 int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tables, hdgc_ctx** out);
 int hdgc_destroy(hdgc_ctx* ctx);
 int hdgc_get_info(const hdgc_ctx* ctx, hdgc_info* info);
@@ -199,6 +210,14 @@ int hdgc_apply_v_host(hdgc_ctx* ctx, const double* u_loc, const double* w, const
                       double* r, void* stream);
 int hdgc_substeps_host(hdgc_ctx* ctx, const double* u_loc, double* w_inout, const double* inflow,
                        double dt, int32_t nsteps, void* stream);
+
+/* Norm-blowup guard: every update kernel (substeps, propagate,
+ * richardson) sets a context flag when it writes a non-finite value.  This
+ * call synchronises `stream`, and returns HDGC_EBLOWUP (clearing the flag) if
+ * any update since the last check blew up, else HDGC_OK.  hdgc_substeps_host
+ * runs it before returning; hdgc_richardson returns HDGC_EBLOWUP on a
+ * non-finite residual norm. */
+int hdgc_check_finite(hdgc_ctx* ctx, void* stream);
 
 const char* hdgc_last_error(void);
 const char* hdgc_version(void);

@@ -20,10 +20,16 @@ SYMBOLS = (
     "hdgc_substeps", "hdgc_transfer", "hdgc_mass_inverse", "hdgc_max_speed",
     "hdgc_apply_v_host", "hdgc_substeps_host", "hdgc_propagate", "hdgc_richardson",
     "hdgc_set_dofmap", "hdgc_gather", "hdgc_scatter", "hdgc_apply_u", "hdgc_set_curved",
-    "hdgc_last_error", "hdgc_version",
+    "hdgc_check_finite", "hdgc_last_error", "hdgc_version",
 )
 
 HDGC_ENOCONV = -5
+HDGC_EBLOWUP = -6
+
+
+class NormBlowupError(FloatingPointError):
+    """An explicit update produced non-finite values (SPEC.md:433 guard)."""
+
 
 _dp = C.POINTER(C.c_double)
 
@@ -91,6 +97,7 @@ def load(path: str = LIB_PATH):
         "hdgc_scatter": ([vp, vp, vp, vp], C.c_int),
         "hdgc_apply_u": ([vp, vp, vp, vp, vp], C.c_int),
         "hdgc_set_curved": ([vp, i32, vp, vp, vp, vp], C.c_int),
+        "hdgc_check_finite": ([vp, vp], C.c_int),
         "hdgc_last_error": ([], C.c_char_p),
         "hdgc_version": ([], C.c_char_p),
     }
@@ -107,4 +114,6 @@ def load(path: str = LIB_PATH):
 def check(rc: int, what: str):
     if rc != 0:
         msg = load().hdgc_last_error().decode(errors="replace")
+        if rc == HDGC_EBLOWUP:
+            raise NormBlowupError(f"{what}: {msg}")
         raise RuntimeError(f"{what} failed (status {rc}): {msg}")

@@ -58,12 +58,21 @@ enum : int {
 // negative minv[T] = -(slot + 1).  The update kernels then store the raw
 // residual row into cres[slot] and curved_fixup_kernel applies the block
 // inverse afterwards (the kernels' own output for those rows is overwritten).
+// Norm-blowup guard ("instability shows as norm blowup caught by
+// a guard"): the update epilogues sum their output row and set *flag when the
+// sum is not finite (one DADD per output value; the atomic only fires on a
+// blow-up).  hdgc_check_finite reads and clears the flag.
 struct StageParams {
   const double* __restrict__ x = nullptr;
   double* __restrict__ rn = nullptr;
   double* __restrict__ cres = nullptr;   // (n_curved, NB) raw residual rows of curved elements
+  int* __restrict__ flag = nullptr;      // blow-up flag (context-owned), set on non-finite output
   double a = 1.0, b = 0.0, c = 0.0, tau = 0.0;
 };
+
+__device__ __forceinline__ void guard_finite(int* flag, double rowsum) {
+  if (flag != nullptr && !isfinite(rowsum)) atomicOr(flag, 1);
+}
 
 // Per-element neighbour code: >= 0: (neighbour element << 2) | neighbour local
 // edge; < 0: boundary facet, slot = -1 - code (row of the inflow array).

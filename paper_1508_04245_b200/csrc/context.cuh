@@ -59,6 +59,8 @@ struct hdgc_ctx {
   double* d_citrans = nullptr;  // (n_curved, nb, nb) I_T (L2 projection), I^T = I_T^T
   double* d_cpiola = nullptr;   // (n_curved, nqv, 4) J/detJ at the volume points
   double* d_cres = nullptr;     // (n_curved, nb) raw residual rows (update kernels -> fix-up)
+  int* d_flag = nullptr;        // (1,) norm-blowup flag set by the update epilogues (StageParams::flag)
+  int* h_flag = nullptr;        // pinned host copy of d_flag
   int64_t bytes = 0;
   int variant = 0;              // 0: thread-per-element (k <= 2), 1: sum-factorised (k >= 3)
   bool pdl = false;             // next update kernel may launch with PDL (set by hdgc_substeps only)

@@ -665,15 +665,18 @@ __device__ __forceinline__ void stage_x(const StageParams& st, double mi, double
                                      const double* part, const double (&wo)[NBS], double* out,
                                      const double* __restrict__ xg, double* rn) {
   const double tm = -st.tau * mi;
-  double acc = 0.0;
+  double acc = 0.0, chk = 0.0;
 #pragma unroll
   for (int m = 0; m < NBS; ++m) {
     const double rv = r[m] + part[m];
     const double xv = __ldg(xg + m);
-    out[m] = fma(st.b, xv, fma(cm, rv, st.a * wo[m]));
+    const double v = fma(st.b, xv, fma(cm, rv, st.a * wo[m]));
+    out[m] = v;
+    chk += v;
     const double res = fma(tm, rv, xv - wo[m]);
     acc = fma(res, res, acc);
   }
+  guard_finite(st.flag, chk);
   if (rn) *rn = acc;
 }
 
@@ -771,8 +774,14 @@ conv2d_sf_kernel(SFParams p) {
       }
       if (MODE == MODE_SUBSTEP) {
         const double cm = p.st.c * mi;
+        double chk = 0.0;
 #pragma unroll
-        for (int m = 0; m < NBS; ++m) wo_s[m] = fma(cm, r[m] + part[m], wo[m]);
+        for (int m = 0; m < NBS; ++m) {
+          const double v = fma(cm, r[m] + part[m], wo[m]);
+          wo_s[m] = v;
+          chk += v;
+        }
+        guard_finite(p.st.flag, chk);
       } else if (MODE == MODE_STAGE) {
         stage_x(p.st, mi, p.st.c * mi, r, part, wo, wo_s, p.st.x + (size_t)T * NB + c * NBS,
                 p.st.rn ? p.st.rn + 2 * (size_t)T + c : nullptr);

@@ -222,22 +222,31 @@ conv2d_thread_kernel(ElemParams p) {
     for (int j = 0; j < NB; ++j) og[j] = r[j];
   } else if (MODE == MODE_SUBSTEP) {
     const double cm = p.st.c * __ldg(p.minv + T);
+    double chk = 0.0;
 #pragma unroll
-    for (int j = 0; j < NB; ++j) og[j] = fma(cm, r[j], w[j]);
+    for (int j = 0; j < NB; ++j) {
+      const double v = fma(cm, r[j], w[j]);
+      og[j] = v;
+      chk += v;
+    }
+    guard_finite(p.st.flag, chk);
   } else if (MODE == MODE_STAGE) {
     const double mi = __ldg(p.minv + T);
     const double cm = p.st.c * mi;
     {
       const double* xg = p.st.x + (size_t)T * NB;
       const double tm = -p.st.tau * mi;
-      double acc0 = 0.0, acc1 = 0.0;
+      double acc0 = 0.0, acc1 = 0.0, chk = 0.0;
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         const double xv = __ldg(xg + j);
-        og[j] = fma(p.st.b, xv, fma(cm, r[j], p.st.a * w[j]));
+        const double v = fma(p.st.b, xv, fma(cm, r[j], p.st.a * w[j]));
+        og[j] = v;
+        chk += v;
         const double res = fma(tm, r[j], xv - w[j]);
         if (j < NBS) acc0 = fma(res, res, acc0); else acc1 = fma(res, res, acc1);
       }
+      guard_finite(p.st.flag, chk);
       if (p.st.rn) {
         p.st.rn[2 * (size_t)T] = acc0;
         p.st.rn[2 * (size_t)T + 1] = acc1;

@@ -91,7 +91,7 @@ inline int dims3_tab(int k) {
 }
 
 // geometry: J (columns = edges), det, Piola J/detJ (9, NT), 6/|detJ|, sign
-__global__ void geometry3d_kernel(const double* __restrict__ V, const int64_t* __restrict__ tet, int nt,
+__global__ void geometry3d_kernel(const double* __restrict__ V, const int64_t* __restrict__ tet, int nt, int nv,
                                   double* __restrict__ piola, double* __restrict__ minv,
                                   double* __restrict__ sgn, int* __restrict__ bad);
 
@@ -617,23 +617,32 @@ conv3d_kernel(Conv3Params p) {
   double* og = p.out + (size_t)T * NB + c * NBS;
   if (MODE == MODE_SUBSTEP) {
     const double cm = p.st.c * __ldg(p.minv + T);
+    double chk = 0.0;
 #pragma unroll
-    for (int m = 0; m < NBS; ++m) og[m] = fma(cm, r[m], W(m));
+    for (int m = 0; m < NBS; ++m) {
+      const double v = fma(cm, r[m], W(m));
+      og[m] = v;
+      chk += v;
+    }
+    guard_finite(p.st.flag, chk);
   } else if (MODE == MODE_STAGE) {
     const double mi = __ldg(p.minv + T);
     const double cm = p.st.c * mi;
     {
       const double* xg = p.st.x + (size_t)T * NB + c * NBS;
       const double tm = -p.st.tau * mi;
-      double acc = 0.0;
+      double acc = 0.0, chk = 0.0;
 #pragma unroll
       for (int m = 0; m < NBS; ++m) {
         const double xv = __ldg(xg + m);
         const double wm = W(m);
-        og[m] = fma(p.st.b, xv, fma(cm, r[m], p.st.a * wm));
+        const double v = fma(p.st.b, xv, fma(cm, r[m], p.st.a * wm));
+        og[m] = v;
+        chk += v;
         const double res = fma(tm, r[m], xv - wm);
         acc = fma(res, res, acc);
       }
+      guard_finite(p.st.flag, chk);
       if (p.st.rn) p.st.rn[3 * (size_t)T + c] = acc;
     }
   } else {

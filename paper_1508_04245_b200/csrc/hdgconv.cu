@@ -5,6 +5,9 @@
 #include <cstdio>
 #include <cstdarg>
 #include <cstring>
+#include <cstdint>
+#include <cmath>
+#include <initializer_list>
 #include <string>
 #include <vector>
 
@@ -105,19 +108,24 @@ __global__ void scatter_kernel(const int32_t* __restrict__ inv, const double* __
 // ---------------------------------------------------------------------------
 // setup kernels (on-device geometry / adjacency precompute)
 
+// mesh validation flag: the first error found wins (kernels run in order
+// geometry -> codes -> check_codes, so the most basic error is reported)
+__device__ __forceinline__ void set_bad(int* bad, int code) { atomicCAS(bad, 0, code); }
+
 // Per-element affine geometry: J = [v1-v0, v2-v0] (columns = edges, mesh2d.py:135-150),
 // Piola factor J/detJ and the V_h mass inverse 2/detJ.
 __global__ void geometry2d_kernel(const double* __restrict__ V, const int64_t* __restrict__ tri,
-                                  int nt, double* __restrict__ piola, double* __restrict__ minv,
+                                  int nt, int nv, double* __restrict__ piola, double* __restrict__ minv,
                                   int* __restrict__ bad) {
   int T = blockIdx.x * blockDim.x + threadIdx.x;
   if (T >= nt) return;
   const int64_t a = tri[3 * (size_t)T], b = tri[3 * (size_t)T + 1], c = tri[3 * (size_t)T + 2];
+  if (a < 0 || a >= nv || b < 0 || b >= nv || c < 0 || c >= nv) { set_bad(bad, 5); return; }
   const double x0 = V[2 * a], y0 = V[2 * a + 1];
   const double j00 = V[2 * b] - x0, j10 = V[2 * b + 1] - y0;
   const double j01 = V[2 * c] - x0, j11 = V[2 * c + 1] - y0;
   const double det = j00 * j11 - j01 * j10;
-  if (!(det > 0.0)) atomicExch(bad, 1);
+  if (!(det > 0.0)) set_bad(bad, 1);
   const double id = 1.0 / det;
   piola[T] = j00 * id;
   piola[(size_t)nt + T] = j01 * id;
@@ -127,19 +135,24 @@ __global__ void geometry2d_kernel(const double* __restrict__ V, const int64_t* _
 }
 
 // 3D: J = [v1-v0, v2-v0, v3-v0], Piola J/detJ (9, NT) row-major, 6/|detJ|, sign(detJ)
-__global__ void hdgc::geometry3d_kernel(const double* __restrict__ V, const int64_t* __restrict__ tet, int nt,
+__global__ void hdgc::geometry3d_kernel(const double* __restrict__ V, const int64_t* __restrict__ tet, int nt, int nv,
                                         double* __restrict__ piola, double* __restrict__ minv,
                                         double* __restrict__ sgn, int* __restrict__ bad) {
   int T = blockIdx.x * blockDim.x + threadIdx.x;
   if (T >= nt) return;
   int64_t v[4];
   for (int i = 0; i < 4; ++i) v[i] = tet[4 * (size_t)T + i];
+  for (int i = 0; i < 4; ++i)
+    if (v[i] < 0 || v[i] >= nv) { set_bad(bad, 5); return; }
+  // conv3d.cuh pairs face point q of both neighbours, which needs every tet's
+  // vertex ids in ascending order (shared faces then have the same vertex order)
+  if (!(v[0] < v[1] && v[1] < v[2] && v[2] < v[3])) { set_bad(bad, 6); return; }
   double J[9];
   for (int c = 0; c < 3; ++c)
     for (int d = 0; d < 3; ++d) J[3 * c + d] = V[3 * v[d + 1] + c] - V[3 * v[0] + c];
   const double det = J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6]) +
                      J[2] * (J[3] * J[7] - J[4] * J[6]);
-  if (!(fabs(det) > 0.0)) atomicExch(bad, 1);
+  if (!(fabs(det) > 0.0)) set_bad(bad, 1);
   const double id = 1.0 / det;
   for (int i = 0; i < 9; ++i) piola[(size_t)i * nt + T] = J[i] * id;
   minv[T] = 6.0 / fabs(det);
@@ -189,21 +202,29 @@ __global__ void scan_kernel(int* __restrict__ a, int n, int* __restrict__ total)
 }
 
 // element-owned neighbour codes from the facet arrays (mesh2d.py:178-207)
+// The code array is pre-filled with CODE_UNSET; every (element, local facet)
+// must be claimed exactly once (atomicExch returns the previous value), and
+// check_codes_kernel flags any slot left unset.
+constexpr int32_t CODE_UNSET = (int32_t)0x80808080;
 __global__ void codes_kernel(const int64_t* __restrict__ fe, const int64_t* __restrict__ fl,
-                             const int* __restrict__ slot, int nfac, int faces_per_elem,
+                             const int* __restrict__ slot, int nfac, int nt, int faces_per_elem,
                              int32_t* __restrict__ code, int* __restrict__ bad) {
   int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nfac) return;
   const int64_t e0 = fe[2 * (size_t)f], e1 = fe[2 * (size_t)f + 1];
   const int64_t l0 = fl[2 * (size_t)f], l1 = fl[2 * (size_t)f + 1];
-  if (e0 < 0 || l0 < 0 || l0 >= faces_per_elem) { atomicExch(bad, 2); return; }
+  if (e0 < 0 || e0 >= nt || l0 < 0 || l0 >= faces_per_elem) { set_bad(bad, 2); return; }
   if (e1 >= 0) {
-    if (l1 < 0 || l1 >= faces_per_elem) { atomicExch(bad, 2); return; }
-    code[e0 * faces_per_elem + l0] = (int32_t)((e1 << 2) | l1);
-    code[e1 * faces_per_elem + l1] = (int32_t)((e0 << 2) | l0);
+    if (e1 >= nt || e1 == e0 || l1 < 0 || l1 >= faces_per_elem) { set_bad(bad, 2); return; }
+    if (atomicExch(&code[e0 * faces_per_elem + l0], (int32_t)((e1 << 2) | l1)) != CODE_UNSET) set_bad(bad, 3);
+    if (atomicExch(&code[e1 * faces_per_elem + l1], (int32_t)((e0 << 2) | l0)) != CODE_UNSET) set_bad(bad, 3);
   } else {
-    code[e0 * faces_per_elem + l0] = -1 - slot[f];
+    if (atomicExch(&code[e0 * faces_per_elem + l0], -1 - slot[f]) != CODE_UNSET) set_bad(bad, 3);
   }
+}
+__global__ void check_codes_kernel(const int32_t* __restrict__ code, size_t n, int* __restrict__ bad) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && code[i] == CODE_UNSET) set_bad(bad, 4);
 }
 
 namespace hdgc {
@@ -253,20 +274,24 @@ __global__ void curved_fixup_kernel(int mode, const int32_t* __restrict__ el, in
   const size_t T = (size_t)el[slot];
   const double* Mi = minv + (size_t)slot * nbs * nbs;
   const double* r = cres + (size_t)slot * nb + comp * nbs;
-  double acc = 0.0;
+  double acc = 0.0, chk = 0.0;
   for (int m = 0; m < nbs; ++m) {
     double s = 0.0;
     for (int l = 0; l < nbs; ++l) s = fma(Mi[m * nbs + l], r[l], s);
     const size_t g = T * nb + comp * nbs + m;
+    double v;
     if (mode == MODE_SUBSTEP) {
-      out[g] = fma(sp.c, s, w[g]);
+      v = fma(sp.c, s, w[g]);
     } else {
       const double xv = sp.x[g];
-      out[g] = fma(sp.b, xv, fma(sp.c, s, sp.a * w[g]));
+      v = fma(sp.b, xv, fma(sp.c, s, sp.a * w[g]));
       const double res = fma(-sp.tau, s, xv - w[g]);
       acc = fma(res, res, acc);
     }
+    out[g] = v;
+    chk += v;
   }
+  guard_finite(sp.flag, chk);
   if (mode == MODE_STAGE && sp.rn) sp.rn[2 * T + comp] = acc;
 }
 
@@ -364,9 +389,10 @@ static int apply_any_(hdgc_ctx* c, int mode, const double* u, const double* w, c
                       const StageParams& sp, bool prep_done, cudaStream_t st);
 static int apply_any(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
                      const StageParams& sp0, bool prep_done, cudaStream_t st) {
-  if (c->n_curved == 0 || (mode != MODE_SUBSTEP && mode != MODE_STAGE))
-    return apply_any_(c, mode, u, w, inflow, out, sp0, prep_done, st);
+  if (mode != MODE_SUBSTEP && mode != MODE_STAGE) return apply_any_(c, mode, u, w, inflow, out, sp0, prep_done, st);
   StageParams sp = sp0;
+  sp.flag = c->d_flag;   // norm-blowup guard of the update epilogues
+  if (c->n_curved == 0) return apply_any_(c, mode, u, w, inflow, out, sp, prep_done, st);
   sp.cres = c->d_cres;
   int rc = apply_any_(c, mode, u, w, inflow, out, sp, prep_done, st);
   return rc ? rc : curved_fixup(c, mode, w, out, sp, st);
@@ -431,6 +457,30 @@ static int maxspeed3(hdgc_ctx* c, const double* u, double* out, cudaStream_t st)
 
 extern "C" int hdgc_destroy(hdgc_ctx* c);
 
+// setup validation flags (bad) -> error text
+static int mesh_error(int bad) {
+  switch (bad) {
+    case 1: return hdgc_set_err(HDGC_EINVAL, "inverted or degenerate element (detJ <= 0 in 2D, detJ = 0 in 3D)");
+    case 2: return hdgc_set_err(HDGC_EINVAL, "invalid facet_elems/facet_local entry (element id or local facet out of range)");
+    case 3: return hdgc_set_err(HDGC_EINVAL, "an (element, local facet) pair appears in more than one facet");
+    case 4: return hdgc_set_err(HDGC_EINVAL, "an (element, local facet) pair is missing from the facet arrays");
+    case 5: return hdgc_set_err(HDGC_EINVAL, "element vertex id out of range [0, n_vertices)");
+    case 6: return hdgc_set_err(HDGC_EINVAL, "3D: every tet's vertex ids must be sorted ascending (shared faces are then "
+                                             "parametrised alike on both sides; facet_perm is not supported)");
+    default: return hdgc_set_err(HDGC_EINVAL, "invalid mesh (code %d)", bad);
+  }
+}
+
+// flag buffers of the norm-blowup guard
+static int alloc_flag(hdgc_ctx* c) {
+  int rc = hdgc_dev_alloc(c, (void**)&c->d_flag, sizeof(int));
+  if (rc) return rc;
+  if (cudaMemset(c->d_flag, 0, sizeof(int)) != cudaSuccess || cudaMallocHost((void**)&c->h_flag, sizeof(int)) != cudaSuccess)
+    return hdgc_set_err(HDGC_ECUDA, "blow-up flag allocation failed");
+  *c->h_flag = 0;
+  return HDGC_OK;
+}
+
 // 3D context: tet mesh (vertices sorted per tet), Dims3<K> tables
 static int create3d(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ctx** out) {
   const int k = tab->k;
@@ -445,6 +495,8 @@ static int create3d(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdg
       !tab->div_modal || !tab->vol_w || !tab->vol_D || !tab->vol_G || !tab->fac_w || !tab->fac_L ||
       !tab->fac_D || !tab->fac_len)
     return hdgc_set_err(HDGC_EINVAL, "null array in descriptor");
+  if (mesh->facet_perm)
+    return hdgc_set_err(HDGC_EINVAL, "facet_perm must be NULL: pass tets with ascending vertex ids instead");
   hdgc_ctx* c = new hdgc_ctx();
   c->dim = 3;
   c->k = k;
@@ -507,20 +559,22 @@ static int create3d(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdg
   SETUP3_TRY(cudaMemcpy(d_fl, mesh->facet_local, sizeof(int64_t) * 2 * NF, cudaMemcpyHostToDevice));
   int* d_misc = d_slot + NF;
   SETUP3_TRY(cudaMemset(d_misc, 0, 2 * sizeof(int)));
+  SETUP3_TRY(cudaMemset(c->d_code, 0x80, NT * 4 * sizeof(int32_t)));   // CODE_UNSET
   {
     const int th = 256;
-    geometry3d_kernel<<<(int)((NT + th - 1) / th), th>>>(d_V, d_tet, (int)NT, c->d_piola, c->d_minv, c->d_sign,
-                                                         d_misc + 1);
+    geometry3d_kernel<<<(int)((NT + th - 1) / th), th>>>(d_V, d_tet, (int)NT, c->nv, c->d_piola, c->d_minv,
+                                                         c->d_sign, d_misc + 1);
     bflag_kernel<<<(int)((NF + th - 1) / th), th>>>(d_fe, (int)NF, d_slot);
     scan_kernel<<<1, 1024>>>(d_slot, (int)NF, d_misc);
-    codes_kernel<<<(int)((NF + th - 1) / th), th>>>(d_fe, d_fl, d_slot, (int)NF, 4, c->d_code, d_misc + 1);
+    codes_kernel<<<(int)((NF + th - 1) / th), th>>>(d_fe, d_fl, d_slot, (int)NF, (int)NT, 4, c->d_code, d_misc + 1);
+    check_codes_kernel<<<(int)((4 * NT + th - 1) / th), th>>>(c->d_code, 4 * NT, d_misc + 1);
     SETUP3_TRY(cudaGetLastError());
   }
   int misc[2];
   SETUP3_TRY(cudaMemcpy(misc, d_misc, sizeof(misc), cudaMemcpyDeviceToHost));
-  if (misc[1] == 1) return fail(hdgc_set_err(HDGC_EINVAL, "degenerate tetrahedron (detJ = 0)"));
-  if (misc[1] == 2) return fail(hdgc_set_err(HDGC_EINVAL, "invalid facet_elems/facet_local entry"));
+  if (misc[1]) return fail(mesh_error(misc[1]));
   c->nbf = misc[0];
+  if ((rc = alloc_flag(c))) return fail(rc);
   if ((rc = setup3(c, tab))) return fail(rc);
   cudaFree(d_V); cudaFree(d_tet); cudaFree(d_fe); cudaFree(d_fl); cudaFree(d_slot);
   *out = c;
@@ -528,9 +582,37 @@ static int create3d(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdg
 #undef SETUP3_TRY
 }
 
+// Device vectors are moved with 16-byte vector loads and TMA bulk copies
+// (cp.async.bulk needs 16-byte aligned global addresses): reject anything
+// else up front instead of faulting (a misaligned-address fault is sticky and
+// destroys the process's CUDA context).
+static bool misaligned(std::initializer_list<const void*> ps) {
+  for (const void* p : ps)
+    if (p && (reinterpret_cast<uintptr_t>(p) & 15u)) return true;
+  return false;
+}
+#define HDGC_ALIGNED(...)                                                                              \
+  do {                                                                                                \
+    if (misaligned({__VA_ARGS__}))                                                                    \
+      return hdgc_set_err(HDGC_EINVAL, "device pointers must be 16-byte aligned (%s)", #__VA_ARGS__); \
+  } while (0)
+
 extern "C" {
 
 const char* hdgc_last_error(void) { return g_err.c_str(); }
+
+int hdgc_check_finite(hdgc_ctx* c, void* stream) {
+  if (!c) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (*c->h_flag == 0) return HDGC_OK;
+  *c->h_flag = 0;
+  CUDA_TRY(cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return hdgc_set_err(HDGC_EBLOWUP, "norm blow-up: an explicit update produced non-finite values "
+                                    "(substep too large for the CFL limit?)");
+}
 const char* hdgc_version(void) { return "hdgconv 0.2 sm_100a fp64"; }
 
 int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ctx** out) {
@@ -606,20 +688,22 @@ int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ct
   SETUP_TRY(cudaMemcpy(d_fl, mesh->facet_local, sizeof(int64_t) * 2 * NF, cudaMemcpyHostToDevice));
   int* d_misc = d_slot + NF;  // [0] = total boundary facets, [1] = bad flag
   SETUP_TRY(cudaMemset(d_misc, 0, 2 * sizeof(int)));
-  SETUP_TRY(cudaMemset(c->d_code, 0x80, NT * 3 * sizeof(int32_t)));  // sentinel: unmatched
+  SETUP_TRY(cudaMemset(c->d_code, 0x80, NT * 3 * sizeof(int32_t)));  // CODE_UNSET
   {
     const int th = 256;
-    geometry2d_kernel<<<(int)((NT + th - 1) / th), th>>>(d_V, d_tri, (int)NT, c->d_piola, c->d_minv, d_misc + 1);
+    geometry2d_kernel<<<(int)((NT + th - 1) / th), th>>>(d_V, d_tri, (int)NT, c->nv, c->d_piola, c->d_minv,
+                                                         d_misc + 1);
     bflag_kernel<<<(int)((NF + th - 1) / th), th>>>(d_fe, (int)NF, d_slot);
     scan_kernel<<<1, 1024>>>(d_slot, (int)NF, d_misc);
-    codes_kernel<<<(int)((NF + th - 1) / th), th>>>(d_fe, d_fl, d_slot, (int)NF, 3, c->d_code, d_misc + 1);
+    codes_kernel<<<(int)((NF + th - 1) / th), th>>>(d_fe, d_fl, d_slot, (int)NF, (int)NT, 3, c->d_code, d_misc + 1);
+    check_codes_kernel<<<(int)((3 * NT + th - 1) / th), th>>>(c->d_code, 3 * NT, d_misc + 1);
     SETUP_TRY(cudaGetLastError());
   }
   int misc[2];
   SETUP_TRY(cudaMemcpy(misc, d_misc, sizeof(misc), cudaMemcpyDeviceToHost));
-  if (misc[1] == 1) return fail(hdgc_set_err(HDGC_EINVAL, "inverted or degenerate element (detJ <= 0)"));
-  if (misc[1] == 2) return fail(hdgc_set_err(HDGC_EINVAL, "invalid facet_elems/facet_local entry"));
+  if (misc[1]) return fail(mesh_error(misc[1]));
   c->nbf = misc[0];
+  if ((rc = alloc_flag(c))) return fail(rc);
   if ((rc = setup_variant(c, tab, h))) return fail(rc);
   cudaFree(d_V); cudaFree(d_tri); cudaFree(d_fe); cudaFree(d_fl); cudaFree(d_slot);
   *out = c;
@@ -634,6 +718,8 @@ int hdgc_destroy(hdgc_ctx* c) {
   cudaFree(c->d_uext); cudaFree(c->d_rn); cudaFree(c->d_sum);
   cudaFree(c->d_dof); cudaFree(c->d_dfac); cudaFree(c->d_inv); cudaFree(c->d_invf); cudaFree(c->d_gl); cudaFree(c->d_rw);
   cudaFree(c->d_celems); cudaFree(c->d_cminv); cudaFree(c->d_citrans); cudaFree(c->d_cpiola); cudaFree(c->d_cres);
+  cudaFree(c->d_flag);
+  if (c->h_flag) cudaFreeHost(c->h_flag);
   if (c->h_sum) cudaFreeHost(c->h_sum);
   if (c->blas) cublasDestroy(static_cast<cublasHandle_t>(c->blas));
   delete c;
@@ -653,12 +739,14 @@ int hdgc_get_info(const hdgc_ctx* c, hdgc_info* info) {
 int hdgc_apply_v(hdgc_ctx* c, const double* u, const double* w, const double* inflow, double* r, void* stream) {
   if (!c || !u || !w || !r) return hdgc_set_err(HDGC_EINVAL, "null argument");
   if (r == u || r == w || r == inflow) return hdgc_set_err(HDGC_EINVAL, "output aliases an input");
+  HDGC_ALIGNED(u, w, inflow, r);
   return apply_any(c, MODE_APPLY, u, w, inflow, r, 0.0, false, (cudaStream_t)stream);
 }
 
 int hdgc_apply_w(hdgc_ctx* c, const double* u, const double* inflow, double* r_w, void* stream) {
   if (!c || !u || !r_w) return hdgc_set_err(HDGC_EINVAL, "null argument");
   if (r_w == u || r_w == inflow) return hdgc_set_err(HDGC_EINVAL, "output aliases an input");
+  HDGC_ALIGNED(u, inflow, r_w);
   cudaStream_t st = (cudaStream_t)stream;
   int rc = transfer(c, 0, u, c->d_scratch, st);
   if (rc) return rc;
@@ -677,6 +765,7 @@ int hdgc_substeps(hdgc_ctx* c, const double* u, double* w, const double* inflow,
   if (!c || !u || !w) return hdgc_set_err(HDGC_EINVAL, "null argument");
   if (nsteps < 0) return hdgc_set_err(HDGC_EINVAL, "nsteps < 0");
   if (w == u || w == inflow) return hdgc_set_err(HDGC_EINVAL, "w aliases an input");
+  HDGC_ALIGNED(u, w, inflow);
   cudaStream_t st = (cudaStream_t)stream;
   double* a = w;
   double* b = c->d_scratch;
@@ -706,6 +795,7 @@ int hdgc_propagate(hdgc_ctx* c, const double* u_prev, const double* u_cur, doubl
   if (scheme != 0 && scheme != 1) return hdgc_set_err(HDGC_EINVAL, "scheme must be 0 (Euler) or 1 (SSP-RK2)");
   if (w == u_cur || w == u_prev || w == inflow) return hdgc_set_err(HDGC_EINVAL, "w aliases an input");
   if (u_prev && !(t_cur != t_prev)) return hdgc_set_err(HDGC_EINVAL, "extrapolation needs t_cur != t_prev");
+  HDGC_ALIGNED(u_prev, u_cur, inflow, w);
   cudaStream_t st = (cudaStream_t)stream;
   const size_t n = (size_t)c->nt * c->nb;
   int rc;
@@ -771,6 +861,7 @@ int hdgc_richardson(hdgc_ctx* c, const double* u, const double* g, const double*
   if (!c || !u || !g || !v) return hdgc_set_err(HDGC_EINVAL, "null argument");
   if (max_iter < 0) return hdgc_set_err(HDGC_EINVAL, "max_iter < 0");
   if (v == u || v == g || v == inflow) return hdgc_set_err(HDGC_EINVAL, "v aliases an input");
+  HDGC_ALIGNED(u, g, inflow, v);
   cudaStream_t st = (cudaStream_t)stream;
   const size_t n = (size_t)c->nt * c->nb, nr = (size_t)c->nt * c->dim;
   int rc;
@@ -792,6 +883,11 @@ int hdgc_richardson(hdgc_ctx* c, const double* u, const double* g, const double*
     CUDA_TRY(cudaMemcpyAsync(c->h_sum, c->d_sum, sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     rn = sqrt(*c->h_sum);
+    if (!std::isfinite(rn)) {
+      // the residual norm sums every updated row: non-finite = norm blow-up
+      hdgc_check_finite(c, stream);
+      return hdgc_set_err(HDGC_EBLOWUP, "richardson: non-finite residual norm at iteration %d (norm blow-up)", it);
+    }
     if (it == 0) r0 = rn;
     if (rn <= rho * r0) { conv = true; break; }
     if (it == max_iter) break;
@@ -875,6 +971,7 @@ int hdgc_transfer(hdgc_ctx* c, int32_t direction, const double* in, double* out,
   if (!c || !in || !out) return hdgc_set_err(HDGC_EINVAL, "null argument");
   if (in == out) return hdgc_set_err(HDGC_EINVAL, "output aliases input");
   if (direction != 0 && direction != 1) return hdgc_set_err(HDGC_EINVAL, "direction must be 0 (I) or 1 (I^T)");
+  HDGC_ALIGNED(in, out);
   return transfer(c, direction, in, out, (cudaStream_t)stream);
 }
 
@@ -980,8 +1077,7 @@ int hdgc_substeps_host(hdgc_ctx* c, const double* u, double* w, const double* in
   }
   if ((rc = hdgc_substeps(c, c->d_hu, c->d_hw, din, dt, nsteps, stream))) return rc;
   CUDA_TRY(cudaMemcpyAsync(w, c->d_hw, vec, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  return HDGC_OK;
+  return hdgc_check_finite(c, stream);   // synchronises the stream
 }
 
 }  // extern "C"

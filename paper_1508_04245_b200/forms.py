@@ -28,7 +28,7 @@ from . import basis as B
 
 __all__ = ["FESpace", "FEField", "ConvectionData", "ConvectionOperator", "operator_for",
            "apply_convection", "apply_convection_W", "apply_convection_U", "apply_transfer", "assemble_mass",
-           "device_tables"]
+           "device_tables", "clear_cache"]
 
 
 # ---------------------------------------------------------------------------
@@ -60,15 +60,15 @@ class FESpace:
     def dofmap(self):
         """Global H(div) dof map (fespace.py), cached per space."""
         from .fespace import build_hdiv_dofmap
-        key = (id(self.mesh), self.k)
-        dm = _DOFMAPS.get(key)
-        if dm is None or dm[0] is not self.mesh:
-            dm = (self.mesh, build_hdiv_dofmap(self.mesh, self.k))
-            _DOFMAPS[key] = dm
-        return dm[1]
+        per_mesh = _DOFMAPS.setdefault(self.mesh, {})
+        dm = per_mesh.get(self.k)
+        if dm is None:
+            dm = per_mesh[self.k] = build_hdiv_dofmap(self.mesh, self.k)
+        return dm
 
 
-_DOFMAPS: dict = {}
+# mesh -> {k: HdivDofMap}; weak keys: an entry goes away with its mesh
+_DOFMAPS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
 @dataclass
@@ -175,9 +175,11 @@ class ConvectionOperator:
     nothing except their outputs.
     """
 
-    def __init__(self, mesh, k: int):
+    def __init__(self, mesh, k: int, weak_mesh: bool = False):
         lib = _lib.load()
-        self.mesh = mesh
+        # operator_for's cache holds contexts by weak mesh reference, so the
+        # context (and its device memory) is released together with its mesh
+        self._mesh = weakref.ref(mesh) if weak_mesh else mesh
         self.k = int(k)
         self.dim = 3 if hasattr(mesh, "tets") else 2
         if self.dim == 3:
@@ -245,6 +247,14 @@ class ConvectionOperator:
     # -- helpers ---------------------------------------------------------------
 
     @property
+    def mesh(self):
+        return self._mesh() if isinstance(self._mesh, weakref.ref) else self._mesh
+
+    def close(self):
+        """Release the device context now (otherwise at garbage collection)."""
+        self._fin()
+
+    @property
     def handle(self):
         return self._h
 
@@ -258,6 +268,10 @@ class ConvectionOperator:
             if not x.is_cuda or x.dtype != torch.float64:
                 raise TypeError(f"{name}: expected a CUDA float64 tensor")
             t = x.contiguous()
+            if t.data_ptr() % 16:
+                # the kernels move rows with 16-byte vector loads and TMA bulk
+                # copies (include/hdgconv.h: pointers must be 16-byte aligned)
+                t = t.clone()
             host = False
         else:
             a = np.ascontiguousarray(x, dtype=np.float64)
@@ -334,10 +348,19 @@ class ConvectionOperator:
         wt, host = self._dev(w, self._vec_shape(), "w")
         it, ip = self._inflow(inflow)
         if not host and wt.data_ptr() != w.data_ptr():
-            raise ValueError("w must be contiguous for the in-place substep loop")
+            raise ValueError("w must be contiguous and 16-byte aligned for the in-place substep loop")
         _lib.check(lib.hdgc_substeps(self._h, C.c_void_p(ut.data_ptr()), C.c_void_p(wt.data_ptr()), ip,
                                      C.c_double(dt), C.c_int32(nsteps), self._stream()), "hdgc_substeps")
-        return wt.cpu().numpy() if host else wt
+        if host:
+            self.check_finite()
+            return wt.cpu().numpy()
+        return wt
+
+    def check_finite(self):
+        """Norm-blowup guard: synchronise the current stream and
+        raise NormBlowupError if any update since the last check wrote a
+        non-finite value (hdgc_check_finite)."""
+        _lib.check(_lib.load().hdgc_check_finite(self._h, self._stream()), "norm-blowup guard")
 
     def substeps_host(self, u: np.ndarray, w: np.ndarray, dt: float, nsteps: int,
                       inflow: Optional[np.ndarray] = None, inplace: bool = False) -> np.ndarray:
@@ -379,12 +402,15 @@ class ConvectionOperator:
         wt, host = self._dev(w, self._vec_shape(), "w")
         it, ip = self._inflow(inflow)
         if not host and wt.data_ptr() != w.data_ptr():
-            raise ValueError("w must be contiguous for the in-place propagation")
+            raise ValueError("w must be contiguous and 16-byte aligned for the in-place propagation")
         _lib.check(lib.hdgc_propagate(self._h, pp, C.c_void_p(ut.data_ptr()), C.c_double(t_prev),
                                       C.c_double(t_cur), C.c_double(t1), C.c_double(ds), C.c_int32(nsteps),
                                       C.c_int32(0 if scheme == "euler" else 1), ip, C.c_void_p(wt.data_ptr()),
                                       self._stream()), "hdgc_propagate")
-        return wt.cpu().numpy() if host else wt
+        if host:
+            self.check_finite()
+            return wt.cpu().numpy()
+        return wt
 
     def richardson(self, u, g, v0, tau: float, ds: float, rho: float = 1e-3, max_iter: int = 500,
                    inflow=None):
@@ -482,18 +508,30 @@ class ConvectionOperator:
         return float(out.item())
 
 
-_CACHE: dict = {}
+# mesh -> {k: ConvectionOperator}.  Weak keys and weak mesh references inside
+# the cached operators: when the caller drops a mesh, its contexts are
+# destroyed (hdgc_destroy via the operator's finalizer) and the device memory
+# is returned, so loops that build many meshes do not accumulate contexts.
+_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
 def operator_for(mesh, k: int) -> ConvectionOperator:
-    """Context cache keyed by (mesh identity, k): building a context uploads
-    tables and runs the geometry precompute, so do it once."""
-    key = (id(mesh), int(k))
-    op = _CACHE.get(key)
-    if op is None or op.mesh is not mesh:
-        op = ConvectionOperator(mesh, k)
-        _CACHE[key] = op
+    """Context cache keyed by (mesh, k): building a context uploads tables and
+    runs the geometry precompute, so do it once per mesh and order."""
+    per_mesh = _CACHE.setdefault(mesh, {})
+    op = per_mesh.get(int(k))
+    if op is None:
+        op = per_mesh[int(k)] = ConvectionOperator(mesh, k, weak_mesh=True)
     return op
+
+
+def clear_cache() -> None:
+    """Destroy every cached context now (operator_for / FESpace.dofmap)."""
+    for per_mesh in list(_CACHE.values()):
+        for op in per_mesh.values():
+            op.close()
+    _CACHE.clear()
+    _DOFMAPS.clear()
 
 
 # ---------------------------------------------------------------------------

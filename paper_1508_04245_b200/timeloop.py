@@ -1,11 +1,12 @@
 """Explicit convection time integration (mirrors ``timeloop`` in SPEC.md:396-496).
 
-* ``cfl_substep(u_max, h_min, k, safety)`` — SPEC.md:438-446, with the
-  BASELINE rule dt = safety * h / (k^2 u_max), safety 0.1.
+* ``cfl_substep(u_max, h_min, k, safety)`` — SPEC.md:438-446:
+  ds = safety * h_min / ((2k+1) u_max).  (BASELINE cfg2's benchmark rule
+  dt = 0.1 h / (k^2 u_max) is ``fields.cfl_dt``; bench.py passes it explicitly.)
 * ``propagate_convection(v0, t1, t2, u_conv, data, scheme, u_prev, ...)`` —
   SPEC.md:429-437: integrates dv/ds + (M^V)^{-1} C^V(u(s)) v = 0
-  over [t1, t2].  scheme "euler" (BASELINE's forward Euler, the default) or
-  "ssprk2" (the SPEC's SSP-RK2); u frozen, or linearly extrapolated from a
+  over [t1, t2].  scheme "ssprk2" (the SPEC's SSP-RK2, the default) or "euler"
+  (BASELINE cfg2's forward Euler); u frozen, or linearly extrapolated from a
   previous field (u_prev at t_prev, u_conv at t_cur).  The whole loop runs on
   the device (hdgc_propagate / hdgc_substeps): one fused apply+update kernel
   per stage, the frozen-velocity prep redone only when u(s) changes.
@@ -24,16 +25,21 @@ __all__ = ["cfl_substep", "propagate_convection", "pseudo_time_solve", "richards
 
 
 def cfl_substep(u_max: float, h_min: float, k: int, safety: float = 0.1, interval: float = math.inf) -> float:
-    """Substep size (SPEC.md:438-446 with the BASELINE k^2 rule)."""
+    """Substep size ds = safety * h_min / ((2k+1) u_max) (SPEC.md:438-446);
+    u_max <= 0 returns the requested interval."""
     if u_max <= 0.0:
         return interval
-    return safety * h_min / (k * k * u_max)
+    return safety * h_min / ((2 * k + 1) * u_max)
 
 
 def propagate_convection(v0, t1: float, t2: float, u_conv: FEField, data: ConvectionData = None,
-                         dt: float = None, safety: float = 0.1, scheme: str = "euler",
-                         u_prev: FEField = None, t_prev: float = None, t_cur: float = None):
+                         dt: float = None, safety: float = 0.1, scheme: str = "ssprk2",
+                         u_prev: FEField = None, t_prev: float = None, t_cur: float = None,
+                         guard: bool = True):
     """Q^{t1->t2} v0 by nsub = ceil((t2-t1)/dt) explicit substeps.
+
+    ``guard``: after the loop, synchronise and raise
+    ``NormBlowupError`` if any substep produced non-finite values.
 
     Returns (v, nsub, ds_used).  ``dt`` defaults to the CFL rule with max|u|
     measured on the device (max over u_prev and u_conv when extrapolating);
@@ -54,12 +60,15 @@ def propagate_convection(v0, t1: float, t2: float, u_conv: FEField, data: Convec
     ds = span / nsub
     inflow = None if data is None else data.inflow
     if scheme == "euler" and u_prev is None:
-        return op.substeps(u_conv.coeffs, v0, ds, nsub, inflow), nsub, ds
-    if u_prev is not None and (t_prev is None or t_cur is None):
-        raise ValueError("extrapolation needs t_prev and t_cur")
-    v = op.propagate(u_conv.coeffs, v0, ds, nsub, inflow, scheme,
-                     None if u_prev is None else u_prev.coeffs,
-                     0.0 if t_prev is None else t_prev, 0.0 if t_cur is None else t_cur, t1)
+        v = op.substeps(u_conv.coeffs, v0, ds, nsub, inflow)
+    else:
+        if u_prev is not None and (t_prev is None or t_cur is None):
+            raise ValueError("extrapolation needs t_prev and t_cur")
+        v = op.propagate(u_conv.coeffs, v0, ds, nsub, inflow, scheme,
+                         None if u_prev is None else u_prev.coeffs,
+                         0.0 if t_prev is None else t_prev, 0.0 if t_cur is None else t_cur, t1)
+    if guard:
+        op.check_finite()
     return v, nsub, ds
 
 

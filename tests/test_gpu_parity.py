@@ -95,7 +95,7 @@ def test_reference_named_entry_points():
     assert rel(rw, O.transfer_IT(m, k, g["r_ld"])) < APPLY_TOL * B.build_bdm_basis(k).cond
     assert rel(apply_transfer("I", g["u"], sp), g["w"]) < 1e-13
     v, nsub, ds = propagate_convection(g["w"], 0.0, float(g["dt"]) * int(g["nsub"]), uf,
-                                       ConvectionData(inflow=inflow), dt=float(g["dt"]))
+                                       ConvectionData(inflow=inflow), dt=float(g["dt"]), scheme="euler")
     assert nsub == int(g["nsub"]) and rel(v, g["w_sub_ld"]) < SUBSTEP_TOL
 
 

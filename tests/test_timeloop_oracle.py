@@ -3,6 +3,8 @@ the SPEC.md timeloop examples, and of the host-side step rules.""
 
 import math
 
+import pytest
+
 import numpy as np
 
 from oracle import convection as O
@@ -99,3 +101,16 @@ def test_step_rules():
     assert TL.richardson_ds(1.0, 0.0, 0.1, 2) == 1.0          # zero velocity: full step
     dtc = TL.cfl_substep(2.0, 0.1, 2)
     assert abs(TL.richardson_ds(1e6, 2.0, 0.1, 2) * 1e6 - dtc) < 1e-6 * dtc
+
+
+def test_cfl_substep_spec_examples():
+    """ds = safety h_min / ((2k+1) u_max); u_max -> 0 gives the
+    interval; halving h_min halves ds."""
+    assert TL.cfl_substep(1.0, 0.1, 2, 0.5) == pytest.approx(0.01, rel=1e-15)
+    assert TL.cfl_substep(0.0, 0.1, 2, 0.5, interval=0.25) == 0.25
+    assert TL.cfl_substep(1.0, 0.05, 2, 0.5) == pytest.approx(0.005, rel=1e-15)
+
+
+def test_propagate_convection_defaults_to_ssprk2():
+    import inspect
+    assert inspect.signature(TL.propagate_convection).parameters["scheme"].default == "ssprk2"

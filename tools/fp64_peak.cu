@@ -78,6 +78,38 @@ __global__ void dmma_m16n8k8(double* out, int iters) {
   if (s == 1234.5) out[0] = s;
 }
 
+// Do DMMA and DFMA share one FP64 pipe?  Even warps run m8n8k4 DMMA chains,
+// odd warps DFMA chains (8x the iterations: 512 vs 64 flops per warp
+// instruction); the combined rate tells whether the two overlap.
+__global__ void mixed_kernel(double* out, int iters, double a, double b) {
+  double s = 0;
+  if (((threadIdx.x >> 5) & 1) == 0) {
+    double av = threadIdx.x * 1e-3, bv = 1.0 + threadIdx.x * 1e-4;
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { c[i][0] = i; c[i][1] = -i; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(av), "d"(bv));
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  } else {
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < 8 * iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], a, b);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i];
+  }
+  if (s == 1234.5) out[0] = s;
+}
+
 template <typename F>
 static float time_it(F launch, int reps) {
   cudaEvent_t e0, e1;
@@ -126,6 +158,14 @@ int main() {
     float ms = time_it([&] { dmma_m16n8k8<8><<<blocks, threads>>>(out, iters); }, 5);
     double flops = 2.0 * 16 * 8 * 8 * 8.0 * iters * blocks * (threads / 32);
     printf(", \"dmma_m16n8k8_tflops\": %.3f", flops / ms / 1e9);
+  }
+  {
+    int blocks = sms * 8; int iters = 2000;
+    float ms = time_it([&] { mixed_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7); }, 5);
+    // half the warps: 8 DMMA x 512 flops per iteration; the other half: 8 x 8 DFMA x 64 flops
+    const double warps = (double)blocks * (threads / 32) / 2;
+    double flops = warps * iters * 8 * 512.0 + warps * 8.0 * iters * 8 * 64.0;
+    printf(", \"mixed_dmma_dfma_tflops\": %.3f", flops / ms / 1e9);
   }
   CK(cudaGetLastError());
   printf("}\n");
