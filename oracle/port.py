@@ -17,6 +17,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "conv_port.c")
+SRC3 = os.path.join(HERE, "conv3d_port.c")
 LIB = os.path.join(HERE, "build", "liboracle_port.so")
 
 _lib = None
@@ -24,10 +25,11 @@ _lib = None
 
 def build(force: bool = False) -> str:
     """gcc -O3 -fopenmp -shared (CPU only; no reference sources involved)."""
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(SRC), os.path.getmtime(SRC3)):
         os.makedirs(os.path.dirname(LIB), exist_ok=True)
         subprocess.check_call(["gcc", "-O3", "-march=x86-64-v3", "-fopenmp", "-shared", "-fPIC",
-                               "-o", LIB, SRC])
+                               "-o", LIB + ".tmp", SRC, SRC3])
+        os.replace(LIB + ".tmp", LIB)
     return LIB
 
 
@@ -43,6 +45,11 @@ def _load():
         _lib.port_apply.restype = C.c_int
         _lib.port_substeps.argtypes = common + [vp, C.c_double, i32, vp, i32]
         _lib.port_substeps.restype = C.c_int
+        common3 = [i32, i32, i32, i32] + [vp] * 9 + [vp] * 3 + [vp, vp, vp]
+        _lib.port3_apply.argtypes = common3 + [vp, i32]
+        _lib.port3_apply.restype = C.c_int
+        _lib.port3_substeps.argtypes = common3 + [vp, C.c_double, i32, vp, i32]
+        _lib.port3_substeps.restype = C.c_int
     return _lib
 
 
@@ -111,4 +118,53 @@ class PortOperator:
         work = np.empty_like(out)
         lib.port_substeps(*self._args(), _p(u), _p(out), _p(inflow), _p(self.minv), C.c_double(dt),
                           int(nsteps), _p(work), self.threads)
+        return out
+
+
+class Port3Operator:
+    """3D (tets) C^V(u; w) on the CPU with `threads` OpenMP threads
+    (oracle/conv3d_port.c; restates oracle/convection3d.py's flux form)."""
+
+    def __init__(self, mesh, k, b3=None, threads=None):
+        from paper_1508_04245_b200 import basis as B2
+        if b3 is None:
+            from paper_1508_04245_b200 import basis3d as b3   # tables only
+        self.k = k
+        self.threads = int(threads or os.cpu_count() or 1)
+        qv = b3.quad_tet(3 * k + 1)
+        qf = B2.quad_triangle(3 * k + 1)
+        D, G = b3.dubiner3_values(k, qv.points, with_grads=True)
+        fD = np.stack([b3.dubiner3_values(k, b3.face_points(f, qf.points)) for f in range(4)])
+        c = np.ascontiguousarray
+        self.tabs = [c(b3.build_bdm3_basis(k).coef), c(qv.weights), c(D), c(G), c(qf.weights),
+                     c(B2.dubiner_values(k, qf.points)), c(fD), c(np.asarray(b3.TET_FACE_AREAS, dtype=float)),
+                     c(np.sign(mesh.affine_det))]
+        self.nqv, self.nf = qv.weights.size, qf.weights.size
+        self.nt = mesh.n_elements
+        nbr, nbf, bsl = mesh.element_neighbours()
+        self.adj = [c(nbr, dtype=np.int32), c(nbf, dtype=np.int32), c(bsl, dtype=np.int32)]
+        self.minv = c(6.0 / np.abs(mesh.affine_det))
+
+    def _args(self):
+        return [self.k, self.nt, self.nqv, self.nf] + [_p(t) for t in self.tabs] + [_p(a) for a in self.adj]
+
+    def apply(self, u, w, inflow=None):
+        lib = _load()
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        inflow = None if inflow is None else np.ascontiguousarray(inflow, dtype=np.float64)
+        r = np.empty_like(w)
+        if lib.port3_apply(*self._args(), _p(u), _p(w), _p(inflow), _p(r), self.threads) != 0:
+            raise ValueError("port3_apply: order too large")
+        return r
+
+    def substeps(self, u, w, dt, nsteps, inflow=None):
+        lib = _load()
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.array(w, dtype=np.float64, copy=True, order="C")
+        inflow = None if inflow is None else np.ascontiguousarray(inflow, dtype=np.float64)
+        work = np.empty_like(out)
+        if lib.port3_substeps(*self._args(), _p(u), _p(out), _p(inflow), _p(self.minv), C.c_double(dt),
+                              int(nsteps), _p(work), self.threads) != 0:
+            raise ValueError("port3_substeps: order too large")
         return out

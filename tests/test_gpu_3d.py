@@ -9,6 +9,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from oracle import convection3d as O3  # noqa: E402
+from oracle import port as P  # noqa: E402
 from paper_1508_04245_b200 import basis3d as B3  # noqa: E402
 from paper_1508_04245_b200 import fields3d as F3  # noqa: E402
 from paper_1508_04245_b200 import mesh3d as M3  # noqa: E402
@@ -76,14 +77,21 @@ def test_cfg5_apply_and_20_substeps():
     inf = F3.inflow_values3(m, k, vp)
     op = ConvectionOperator(m, k)
     r = op.apply(dev(u), dev(w), dev(inf)).cpu().numpy()
-    ref = O3.apply_convection3_flux_form(m, k, u, w, inf, dtype=np.float64)
-    assert rel(r, ref) < APPLY_TOL
-    # 20 substeps: full-size invariants (constants stay put) + a 4^3 sub-problem vs the oracle
+    port = P.Port3Operator(m, k)                  # OpenMP C port of the flux-form oracle
+    assert rel(r, port.apply(u, w, inf)) < APPLY_TOL
+    rr = op.apply(dev(u), dev(w_rand := np.random.default_rng(3).standard_normal(w.shape)), dev(inf))
+    assert rel(rr, port.apply(u, w_rand, inf)) < APPLY_TOL
+    # 20 forward-Euler substeps at full size vs the port (north star: <= 1e-10)
+    dt = 0.1 * m.h_min() / (k * k * op.max_speed(dev(u)))
+    wd = dev(w)
+    op.substeps(dev(u), wd, dt, 20, dev(inf))
+    op.check_finite()
+    assert rel(wd, port.substeps(u, w, dt, 20, inf)) < SUBSTEP_TOL
+    # full-size invariant: constants stay put
     nbs = B3.nbs3_of(k)
     c = np.zeros_like(w)
     c[:, 0] = 1.0
     cd = dev(c)
-    dt = 0.1 * m.h_min() / (k * k * op.max_speed(dev(u)))
     op.substeps(dev(u), cd, dt, 20, None)
     assert np.abs(cd.cpu().numpy() - c).max() < 1e-10
 
@@ -119,3 +127,20 @@ def test_pdl_batch_bitwise_equals_single_substeps_3d():
     for _ in range(n):
         one = op.substeps(ud, one, dt, 1)
     assert torch.equal(batch, one)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_wind_inflow_20_substeps_vs_port(k):
+    """Inflow faces (uniform wind through the cube): apply + 20 substeps vs the C port."""
+    m = M3.generate_cube(8)
+    vp = F3.VectorPotential(3, 11, (0.6, -0.3, 0.4))
+    u = F3.interpolate_curl3(m, k, vp)
+    w = F3.transfer_I3_host(m, k, u)
+    inf = F3.inflow_values3(m, k, vp)
+    op = ConvectionOperator(m, k)
+    port = P.Port3Operator(m, k)
+    assert rel(op.apply(dev(u), dev(w), dev(inf)), port.apply(u, w, inf)) < APPLY_TOL
+    dt = 0.1 * m.h_min() / (k * k * op.max_speed(dev(u)))
+    wd = dev(w)
+    op.substeps(dev(u), wd, dt, 20, dev(inf))
+    assert rel(wd, port.substeps(u, w, dt, 20, inf)) < SUBSTEP_TOL
