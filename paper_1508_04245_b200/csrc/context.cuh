@@ -35,6 +35,8 @@ struct hdgc_ctx {
   double* d_sign = nullptr;     // (NT,) sign(detJ) (3D: sorted-vertex tets)
   double* d_ftab = nullptr;     // facet tables fw | fD (sum-factorised variant)
   double* d_afrag = nullptr;    // DMMA A fragments of [coef ; divm] (tile prep, k = 3..6)
+  double* d_mprep = nullptr;    // modal frozen-velocity prep [tile][MP][16] (conv2d_sfm.cuh)
+  bool modal = false;           // the sum-factorised variant uses the modal prep + conv2d_sfm_kernel
   // host-variant staging (lazily allocated)
   double* d_hu = nullptr;
   double* d_hw = nullptr;

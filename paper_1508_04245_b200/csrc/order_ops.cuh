@@ -6,6 +6,7 @@
 #include "context.cuh"
 #include "conv2d_thread.cuh"
 #include "conv2d_sf.cuh"
+#include "conv2d_sfm.cuh"
 
 namespace hdgc {
 
@@ -150,8 +151,37 @@ int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st) 
 }
 
 // frozen-velocity prep rows (alpha | beta | gamma | s) into c->d_prep
+// orders that run the modal-prep variant (conv2d_sfm.cuh); HDGC_MODAL=0 turns
+// it off, HDGC_MODAL=<digits> selects the orders (development A/B switch)
+template <int K>
+bool modal_enabled() {
+  if constexpr (K < 3 || K > 6) {
+    return false;
+  } else {
+    // default off: measured at cfg2 (k = 4, 131k triangles) the modal kernel
+    // moves 106 MB per launch instead of 188 MB but executes 1.34 GFLOP
+    // instead of 0.92 and runs 80-86 us against 59 us
+    const char* e = getenv("HDGC_MODAL");
+    if (!e) return false;
+    for (const char* q = e; *q; ++q)
+      if (*q - '0' == K) return true;
+    return false;
+  }
+}
+
 template <int K>
 int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
+  if constexpr (K >= 3 && K <= 6) {
+    if (c->modal) {
+      const int smem = PrepMma<K>::SMEM * (int)sizeof(double);
+      if (smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(prep_modal2d_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      prep_modal2d_kernel<K><<<(c->nt + 31) / 32, 32 * SF<K>::N, smem, st>>>(c->d_tab, c->d_afrag, u, c->d_minv,
+                                                                           c->nt, c->d_mprep);
+      CUDA_TRY(cudaGetLastError());
+      return HDGC_OK;
+    }
+  }
   // Measured per launch at 131072 elements (ncu, cold): k=3 the fused
   // thread-per-element kernel (24 us; tile 39 us); k>=4 the tile kernel with
   // its DMMA modal stage (k=4 47 us vs fused 84; k=5 87 vs DGEMM 41 + rows 78;
@@ -205,6 +235,31 @@ int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double
     p.out = out;
     p.st = sp;
     p.nt = c->nt;
+    if constexpr (K <= 6) {
+      // three-warp kernel (conv2d_sfm.cuh): modal prep, or (HDGC_SFM3=1) the point prep
+      static const bool sfm3 = [] { const char* e = getenv("HDGC_SFM3"); return e && e[0] == '1'; }();
+      if (c->modal || sfm3) {
+        using S = SFM<K>;
+        const int blocks = (c->nt + S::EPB - 1) / S::EPB;
+        auto launch = [&](auto kern, int smem) -> int {
+          if (smem > 48 * 1024)
+            CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          CUDA_TRY(launch_maybe_pdl(kern, blocks, S::THREADS, smem, st, c->pdl, p));
+          return HDGC_OK;
+        };
+        if (c->modal) {
+          p.prep = c->d_mprep;
+          const int smem = S::template L<true>::SMEM_DOUBLES * (int)sizeof(double);
+          if (mode == MODE_SUBSTEP) return launch(conv2d_sfm_kernel<K, MODE_SUBSTEP, true>, smem);
+          if (mode == MODE_STAGE) return launch(conv2d_sfm_kernel<K, MODE_STAGE, true>, smem);
+          return launch(conv2d_sfm_kernel<K, MODE_APPLY, true>, smem);
+        }
+        const int smem = S::template L<false>::SMEM_DOUBLES * (int)sizeof(double);
+        if (mode == MODE_SUBSTEP) return launch(conv2d_sfm_kernel<K, MODE_SUBSTEP, false>, smem);
+        if (mode == MODE_STAGE) return launch(conv2d_sfm_kernel<K, MODE_STAGE, false>, smem);
+        return launch(conv2d_sfm_kernel<K, MODE_APPLY, false>, smem);
+      }
+    }
     const int smem = F::SMEM_DOUBLES * (int)sizeof(double);
     const int blocks = (c->nt + F::EPB - 1) / F::EPB;
     auto launch = [&](auto kern) -> int {
@@ -281,10 +336,18 @@ int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& 
     int rc = hdgc_dev_alloc(c, (void**)&c->d_ftab, sizeof(double) * F::TAB_PAD);
     if (rc) return rc;
     CUDA_TRY(cudaMemcpy(c->d_ftab, ft.data(), sizeof(double) * F::TAB_PAD, cudaMemcpyHostToDevice));
-    rc = hdgc_dev_alloc(c, (void**)&c->d_prep, sizeof(double) * (size_t)((c->nt + 15) / 16) * F::PREP_TILE);
-    if (rc) return rc;
-    CUDA_TRY(cudaMemset(c->d_prep, 0, sizeof(double) * (size_t)((c->nt + 15) / 16) * F::PREP_TILE));
-    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyToSymbol(c_fw, &packed[D::OFF_FW], sizeof(double) * F::NF));
+    if constexpr (K >= 4 && K <= 6) c->modal = modal_enabled<K>();
+    if (c->modal) {
+      const size_t n = (size_t)((c->nt + 31) / 32) * 2 * SFM<K>::MTILE;   // whole 32-element prep CTAs
+      rc = hdgc_dev_alloc(c, (void**)&c->d_mprep, sizeof(double) * n);
+      if (rc) return rc;
+      CUDA_TRY(cudaMemset(c->d_mprep, 0, sizeof(double) * n));
+    } else {
+      rc = hdgc_dev_alloc(c, (void**)&c->d_prep, sizeof(double) * (size_t)((c->nt + 15) / 16) * F::PREP_TILE);
+      if (rc) return rc;
+      CUDA_TRY(cudaMemset(c->d_prep, 0, sizeof(double) * (size_t)((c->nt + 15) / 16) * F::PREP_TILE));
+    }
     c->variant = 1;
     return HDGC_OK;
   } else {
