@@ -155,8 +155,11 @@ int hdgc_propagate(hdgc_ctx* ctx, const double* u_prev, const double* u_cur, dou
  *   res_i = g - v_i - tau M^-1 C v_i,  v_{i+1} = v_i + ds res_i,
  * stopping at the first i with ||res_i||_2 <= rho ||res_0||_2 (v_inout <- v_i,
  * *iters = i).  Returns HDGC_ENOCONV when i reaches max_iter first (v_inout =
- * v_max_iter).  Synchronises `stream` once per iteration to read the norm;
- * the norm is a fixed-order (deterministic) reduction. */
+ * v_max_iter).  The stopping test runs on the device (a fixed-order,
+ * deterministic reduction of the residual norm raises a stop flag that the
+ * iterations queued after it honour), so the host does not wait per
+ * iteration: it queues iterations in chunks and checks the flag once per
+ * chunk, one chunk behind.  Returns HDGC_EBLOWUP on a non-finite norm. */
 int hdgc_richardson(hdgc_ctx* ctx, const double* u_loc, const double* g, const double* inflow, double tau,
                     double ds, double rho, int32_t max_iter, double* v_inout, int32_t* iters,
                     double* res0, double* res_final, void* stream);

@@ -67,8 +67,39 @@ struct StageParams {
   double* __restrict__ rn = nullptr;
   double* __restrict__ cres = nullptr;   // (n_curved, NB) raw residual rows of curved elements
   int* __restrict__ flag = nullptr;      // blow-up flag (context-owned), set on non-finite output
+  // device-side Richardson stop (hdgc_richardson): when *stop != 0 the update
+  // kernel returns at entry without touching its output (the iteration has
+  // converged on the device; later queued iterations are no-ops)
+  const int* stop = nullptr;
+  // sum-factorised kernels (no curved elements): per-CTA residual partials
+  // (rich_cta_partial) instead of per-(element, component) sums into rn
+  double* rpart = nullptr;
   double a = 1.0, b = 0.0, c = 0.0, tau = 0.0;
 };
+
+// Richardson residual norm, part 1 (sum-factorised STAGE kernels): one whole
+// warp of every CTA sums its lanes' squared residuals in a fixed xor-tree
+// order and stores the CTA partial; richardson_final_kernel (launched with PDL
+// right after) adds the partials in index order and takes the stop decision.
+__device__ __forceinline__ double warp_sum_fixed(double a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  return a;
+}
+__device__ __forceinline__ void rich_cta_partial(const StageParams& st, double acc) {
+  acc = warp_sum_fixed(acc);
+  if ((threadIdx.x & 31) == 0) st.rpart[blockIdx.x] = acc;
+}
+
+__device__ __forceinline__ bool stage_stopped(const StageParams& st) {
+  if (st.stop == nullptr) return false;
+  int v;
+  asm volatile("ld.global.relaxed.gpu.b32 %0, [%1];\n" : "=r"(v) : "l"(st.stop) : "memory");
+  return v != 0;
+}
+// the same flag as a plain L2 load the compiler may schedule early and consume
+// late (call after griddepcontrol.wait: the flag is the previous kernel's output)
+__device__ __forceinline__ int stage_stop_flag(const StageParams& st) { return st.stop ? __ldcg(st.stop) : 0; }
 
 __device__ __forceinline__ void guard_finite(int* flag, double rowsum) {
   if (flag != nullptr && !isfinite(rowsum)) atomicOr(flag, 1);
@@ -124,9 +155,9 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // when pdl is set (the caller guarantees the previous kernel on st is an
 // update kernel of the same batch and nothing before pdl_wait() reads what it
 // writes).
-template <class P>
-inline cudaError_t launch_maybe_pdl(void (*kern)(P), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-                                    bool pdl, const P& p) {
+template <class... P, class... A>
+inline cudaError_t launch_maybe_pdl(void (*kern)(P...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                                    bool pdl, const A&... p) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -137,7 +168,7 @@ inline cudaError_t launch_maybe_pdl(void (*kern)(P), unsigned grid, unsigned blo
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, p);
+  return cudaLaunchKernelEx(&cfg, kern, p...);
 }
 
 }  // namespace hdgc

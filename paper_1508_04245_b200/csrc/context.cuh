@@ -21,6 +21,17 @@ int hdgc_set_err(int code, const char* fmt, ...);
                           __LINE__);                                                          \
   } while (0)
 
+// one captured substep batch (hdgc_substeps), keyed by its arguments
+struct hdgc_graph {
+  const double* u = nullptr;
+  const double* w = nullptr;
+  const double* inflow = nullptr;
+  uint64_t dt_bits = 0;
+  int nsteps = 0;
+  cudaGraphExec_t exec = nullptr;
+};
+constexpr int HDGC_GRAPH_CACHE = 4;
+
 struct hdgc_ctx {
   int dim = 2, k = 0, nb = 0, nbs = 0, nqv = 0, nf = 0;
   int nt = 0, nf_facets = 0, nbf = 0, nv = 0;
@@ -44,8 +55,16 @@ struct hdgc_ctx {
   double* d_hin = nullptr;
   double* d_uext = nullptr;     // (NT, nb) extrapolated velocity (propagate, lazily allocated)
   double* d_rn = nullptr;       // (NT, dim) residual sums of squares (richardson)
-  double* d_sum = nullptr;      // (1,) reduced norm^2
-  double* h_sum = nullptr;      // pinned host copy of d_sum
+  double* d_rpart = nullptr;    // (RED_CTAS,) Richardson reduction partials
+  double* d_fpart = nullptr;    // Richardson CTA partials of the sum-factorised STAGE kernels
+  int* d_ctl = nullptr;         // (4,) Richardson device control block (stop, iteration, blow-up, counter)
+  double* d_norms = nullptr;    // (n_norms,) residual norm per iteration
+  int n_norms = 0;
+  int* h_ctl = nullptr;         // pinned (12,) control-block copies (two chunk slots + final)
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  hdgc_graph graphs[HDGC_GRAPH_CACHE];  // captured substep batches (LRU)
+  int graph_next = 0;
+  cudaStream_t cap_stream = nullptr;    // private stream the batches are captured on
   int64_t ndof = 0;             // global H(div) dof map (hdgc_set_dofmap)
   int32_t* d_dof = nullptr;     // (NT, nb) global dof of each local dof
   double* d_dfac = nullptr;     // (NT, nb) local = factor * global

@@ -100,6 +100,13 @@ struct SF {
   // instead of runtime-indexed constant loads, which ptxas hoists into registers)
   static constexpr int SM_BT = SM_FD + TAB_PAD;
   static constexpr int SMEM_DOUBLES = SM_BT + (SMBT ? 2 * N * NBS : 0);
+  // STAGE mode adds the x tile [EPB][NB] (bulk-copied with w) after SMEM_DOUBLES
+  static constexpr int SM_X = SMEM_DOUBLES;
+#ifndef HDGC_XTILE
+#define HDGC_XTILE 1
+#endif
+  static constexpr bool XTILE = HDGC_XTILE;
+  static constexpr int smem_doubles(int mode) { return SMEM_DOUBLES + (mode == 3 && XTILE ? EPB * NB : 0); }
 };
 
 // The constant-bank tables of the order compiled in this translation unit
@@ -661,7 +668,7 @@ __device__ __forceinline__ void sf_rows_ring(const double* wc, const double* __r
 // stage epilogue with the extra vector x (SSP-RK2 second stage, Richardson):
 // out = a w + b x + c minv r, optional residual sum of squares (StageParams)
 template <int NBS>
-__device__ __forceinline__ void stage_x(const StageParams& st, double mi, double cm, const double (&r)[NBS],
+__device__ __forceinline__ double stage_x(const StageParams& st, double mi, double cm, const double (&r)[NBS],
                                      const double* part, const double (&wo)[NBS], double* out,
                                      const double* __restrict__ xg, double* rn) {
   const double tm = -st.tau * mi;
@@ -669,7 +676,7 @@ __device__ __forceinline__ void stage_x(const StageParams& st, double mi, double
 #pragma unroll
   for (int m = 0; m < NBS; ++m) {
     const double rv = r[m] + part[m];
-    const double xv = __ldg(xg + m);
+    const double xv = xg[m];
     const double v = fma(st.b, xv, fma(cm, rv, st.a * wo[m]));
     out[m] = v;
     chk += v;
@@ -678,6 +685,7 @@ __device__ __forceinline__ void stage_x(const StageParams& st, double mi, double
   }
   guard_finite(st.flag, chk);
   if (rn) *rn = acc;
+  return acc;
 }
 
 // Two warps per CTA on one tile of EPB = 16 elements: warp 0 computes the
@@ -706,6 +714,7 @@ conv2d_sf_kernel(SFParams p) {
   double* s_fD = sm + F::SM_FD;            // edge trace maps [3][RSTR]
   const double* C = sf_tab<K>();
 
+  double* s_x = sm + F::SM_X;              // STAGE: x tile [EPB][NB]
   const int T0 = blockIdx.x * EPB;
   const int nel = min(EPB, p.nt - T0);
   double2* s_BT = reinterpret_cast<double2*>(sm + F::SM_BT);
@@ -720,8 +729,10 @@ conv2d_sf_kernel(SFParams p) {
     const uint32_t bp = F::RING ? 0u : (uint32_t)(F::PREP_TILE * sizeof(double));
     const uint32_t bw = (uint32_t)(nel * NB * sizeof(double));
     const uint32_t bt = (uint32_t)(F::TAB_PAD * sizeof(double));
-    mbar_arrive_expect_tx(bar, bp + bw + bt);
+    mbar_arrive_expect_tx(bar, bp + bw + bt + (MODE == MODE_STAGE && F::XTILE ? bw : 0u));
     if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
+    if (MODE == MODE_STAGE && F::XTILE)
+      bulk_g2s(s_x, p.st.x + (size_t)T0 * NB, bw, bar);   // x is not the previous kernel's output
 #ifdef HDGC_L2PF
     // warm L2 with the prep tile of the CTA that will likely follow on this SM
     {
@@ -755,12 +766,15 @@ conv2d_sf_kernel(SFParams p) {
     // ===================== volume warp =====================
     const double mi = (MODE == MODE_SUBSTEP || MODE == MODE_STAGE) && active ? __ldg(p.minv + T) : 0.0;
     pdl_wait();
+    const int stopped = MODE == MODE_STAGE ? stage_stop_flag(p.st) : 0;   // (latency hidden by the tile wait)
     pdl_trigger();
     mbar_wait(bar, 0);
+    if (stopped) return;   // converged Richardson iteration: queued after the stop, writes nothing
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
     if (F::RING) sf_rows_ring<K>(wc, gtile, s_prep, active ? le : 0, lane, N - F::FACET_ROWS, r, s_BT);
     else sf_rows<K, 0, N - F::FACET_ROWS>(wc, row, r, s_BT);
     asm volatile("bar.sync 1, 64;\n" ::: "memory");   // (A) facet partial r ready, in-tile w reads done
+    double racc = 0.0;   // STAGE: this lane's residual sum of squares
     if (active) {
       double* wo_s = s_w + le * NB + c * NBS;
       double wo[NBS];
@@ -783,8 +797,9 @@ conv2d_sf_kernel(SFParams p) {
         }
         guard_finite(p.st.flag, chk);
       } else if (MODE == MODE_STAGE) {
-        stage_x(p.st, mi, p.st.c * mi, r, part, wo, wo_s, p.st.x + (size_t)T * NB + c * NBS,
-                p.st.rn ? p.st.rn + 2 * (size_t)T + c : nullptr);
+        racc = stage_x(p.st, mi, p.st.c * mi, r, part, wo, wo_s,
+                       (F::XTILE ? s_x : p.st.x + (size_t)T0 * NB) + le * NB + c * NBS,
+                       p.st.rn ? p.st.rn + 2 * (size_t)T + c : nullptr);
       } else {
 #pragma unroll
         for (int m = 0; m < NBS; ++m) wo_s[m] = r[m] + part[m];
@@ -796,14 +811,17 @@ conv2d_sf_kernel(SFParams p) {
       bulk_s2g(p.out + (size_t)T0 * NB, s_w, (uint32_t)(nel * NB * sizeof(double)));
       bulk_wait_read();
     }
+    if (MODE == MODE_STAGE && p.st.rpart) rich_cta_partial(p.st, racc);
   } else {
     // ===================== facet warp =====================
     int codes[3];
 #pragma unroll
     for (int ed = 0; ed < 3; ++ed) codes[ed] = active ? __ldg(p.code + (size_t)T * 3 + ed) : -1;
     pdl_wait();   // halo gathers below read the previous kernel's w
+    const int stopped = MODE == MODE_STAGE ? stage_stop_flag(p.st) : 0;
     pdl_trigger();
     mbar_wait(bar, 0);
+    if (stopped) return;
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
     double* halo = part;
     int halo_edge = -1;

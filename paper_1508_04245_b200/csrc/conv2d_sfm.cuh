@@ -251,8 +251,10 @@ conv2d_sfm_kernel(SFParams p) {
   if (warp < S::NVW) {
     // ===================== volume warps =====================
     pdl_wait();
+    const int stopped = MODE == MODE_STAGE ? stage_stop_flag(p.st) : 0;   // converged Richardson iteration
     pdl_trigger();
     mbar_wait(bar, 0);
+    if (stopped) return;
     const double* wc = s_w + lc * NB + c * NBS;
     const int b0 = warp == 0 ? 0 : S::RB, b1 = warp == 0 ? S::RB : N;
     auto rows = [&](const auto& wv) {
@@ -293,6 +295,7 @@ conv2d_sfm_kernel(SFParams p) {
 #pragma unroll
       for (int m = 0; m < NBS; ++m) wo[m] = wc[m];
     }
+    double racc = 0.0;   // STAGE: this lane's residual sum of squares
     if (active) {
       const double mi = (MODE == MODE_SUBSTEP || MODE == MODE_STAGE)
                             ? (MODAL ? mod[S::S_MI * EPB] : __ldg(p.minv + T)) : 0.0;
@@ -318,8 +321,8 @@ conv2d_sfm_kernel(SFParams p) {
         }
         guard_finite(p.st.flag, chk);
       } else if (MODE == MODE_STAGE) {
-        stage_x(p.st, mi, p.st.c * mi, r, part, wo, wo_s, p.st.x + (size_t)T * NB + c * NBS,
-                p.st.rn ? p.st.rn + 2 * (size_t)T + c : nullptr);
+        racc = stage_x(p.st, mi, p.st.c * mi, r, part, wo, wo_s, p.st.x + (size_t)T * NB + c * NBS,
+                       p.st.rn ? p.st.rn + 2 * (size_t)T + c : nullptr);
       } else {
 #pragma unroll
         for (int m = 0; m < NBS; ++m) wo_s[m] = r[m] + part[m];
@@ -331,14 +334,17 @@ conv2d_sfm_kernel(SFParams p) {
       bulk_s2g(p.out + (size_t)T0 * NB, s_w, (uint32_t)(nel * NB * sizeof(double)));
       bulk_wait_read();
     }
+    if (MODE == MODE_STAGE && p.st.rpart) rich_cta_partial(p.st, racc);
   } else {
     // ===================== facet warp =====================
     int codes[3];
 #pragma unroll
     for (int ed = 0; ed < 3; ++ed) codes[ed] = active ? __ldg(p.code + (size_t)T * 3 + ed) : -1;
     pdl_wait();   // halo gathers below read the previous kernel's w
+    const int stopped = MODE == MODE_STAGE ? stage_stop_flag(p.st) : 0;
     pdl_trigger();
     mbar_wait(bar, 0);
+    if (stopped) return;
     const double* wc = s_w + lc * NB + c * NBS;
     const double* fx = mod + S::S_FX * EPB;          // edge flux coefficients, edge e at fx[e NE EPB]
     // inflow edges of this element: any point with F < 0 (modal: F from the edge dofs)

@@ -43,6 +43,7 @@ conv2d_thread_kernel(ElemParams p) {
   static_assert(K == HDGC_ORDER && K <= 2, "thread variant: k <= 2, tables per translation unit");
   using D = Dims<K>;
   constexpr int NB = D::NB, NBS = D::NBS, NBS1 = D::NBS1, NE = D::NE, NF = D::NF, NQV = D::NQV;
+  if (MODE == MODE_STAGE && stage_stopped(p.st)) return;   // converged Richardson iteration
   const double* coef = c_th + D::OFF_COEF;
   const double* divm = c_th + D::OFF_DIVM;
   const double* vw = c_th + D::OFF_VW;

@@ -388,6 +388,7 @@ __global__ void __launch_bounds__(96, HDGC_3D_MINB)
 conv3d_kernel(Conv3Params p) {
   using D = Dims3<K>;
   constexpr int NB = D::NB, NBS = D::NBS, NQ = D::NQ, NF = D::NF;
+  if (MODE == MODE_STAGE && stage_stopped(p.st)) return;   // converged Richardson iteration
   const int c = threadIdx.x / D::EPB;
   const int T0 = blockIdx.x * D::EPB + (threadIdx.x % D::EPB);
   const bool active = T0 < p.nt;

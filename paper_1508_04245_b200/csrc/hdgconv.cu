@@ -70,22 +70,89 @@ __global__ void axpby_kernel(const double* __restrict__ x, const double* __restr
   if (i < n) out[i] = fma(a, x[i], b * y[i]);
 }
 
-// *out = sum v[0..n) in a fixed order (one CTA of 1024 threads: strided partial
-// sums, then a fixed shuffle/smem tree), so residual norms are bitwise
-// reproducible run to run.
-__global__ void __launch_bounds__(1024) sum_kernel(const double* __restrict__ v, size_t n, double* out) {
-  __shared__ double red[32];
-  double a = 0.0;
-  for (size_t i = threadIdx.x; i < n; i += 1024) a += v[i];
+// Richardson control on the device (hdgc_richardson).  ctl (ints): [0] stop
+// (converged or blown up), [1] iteration it stopped at, [2] blow-up, [3]
+// arrival counter of the reduction.  Each iteration's reduction sums the
+// per-(element, component) residual sums rn in a fixed order — RED_CTAS
+// contiguous chunks, each a fixed block tree, then the chunk partials in
+// index order by whichever CTA arrives last — so norms, stop decisions and
+// iteration counts are bitwise reproducible; it stores ||res_it|| into
+// norms[it] and raises the stop flag at the first it with
+// ||res_it|| <= rho ||res_0|| (or a non-finite norm).  Update kernels queued
+// after the flag is raised return at entry (StageParams::stop).
+constexpr int RED_CTAS = 256, RED_THREADS = 256;
+
+__device__ __forceinline__ double block_sum_fixed(double a, double* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
   __syncthreads();
+  a = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
   if (threadIdx.x < 32) {
-    a = red[threadIdx.x];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (threadIdx.x == 0) *out = a;
+  }
+  return a;   // valid in thread 0
+}
+
+__global__ void __launch_bounds__(RED_THREADS) richardson_reduce_kernel(const double* __restrict__ rn, size_t n, int it,
+                                                                        double rho, double* part, double* norms,
+                                                                        int* ctl) {
+  __shared__ double red[RED_THREADS / 32];
+  __shared__ int last;
+  if (*(volatile int*)ctl != 0) return;   // stopped at an earlier iteration: no-op
+  const size_t per = (n + gridDim.x - 1) / gridDim.x;
+  const size_t b0 = min(n, (size_t)blockIdx.x * per), b1 = min(n, b0 + per);
+  double a = 0.0;
+  for (size_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) a += rn[i];
+  a = block_sum_fixed(a, red);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = a;
+    __threadfence();
+    last = atomicAdd(&ctl[3], 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __syncthreads();
+  a = threadIdx.x < gridDim.x ? ((volatile double*)part)[threadIdx.x] : 0.0;
+  a = block_sum_fixed(a, red);
+  if (threadIdx.x == 0) {
+    const double r = sqrt(a);
+    norms[it] = r;
+    ctl[3] = 0;
+    const double r0 = it == 0 ? r : norms[0];
+    if (!isfinite(r)) {
+      ctl[2] = 1; ctl[1] = it; __threadfence(); ctl[0] = 1;
+    } else if (r <= rho * r0) {
+      ctl[1] = it; __threadfence(); ctl[0] = 1;
+    }
+  }
+}
+
+// Richardson residual norm, part 2 (fused path): one CTA adds the CTA
+// partials of the STAGE kernel before it in index order and takes the stop
+// decision.  Launched with PDL: it lets the next STAGE kernel launch at once
+// (that one stages its prep / x tiles, then waits in griddepcontrol.wait for
+// this kernel), and itself waits for the STAGE kernel to complete.
+__global__ void __launch_bounds__(1024) richardson_final_kernel(const double* __restrict__ part, int n, int it,
+                                                                double rho, double* norms, int* ctl) {
+  __shared__ double red[32];
+  pdl_trigger();
+  pdl_wait();
+  if (*(volatile int*)ctl != 0) return;   // stopped at an earlier iteration: no-op
+  double a = 0.0;
+  for (int i = threadIdx.x; i < n; i += 1024) a += part[i];
+  a = block_sum_fixed(a, red);
+  if (threadIdx.x == 0) {
+    const double r = sqrt(a);
+    norms[it] = r;
+    const double r0 = it == 0 ? r : norms[0];
+    if (!isfinite(r)) {
+      ctl[2] = 1; ctl[1] = it; ctl[0] = 1;
+    } else if (r <= rho * r0) {
+      ctl[1] = it; ctl[0] = 1;
+    }
   }
 }
 
@@ -270,6 +337,7 @@ __global__ void curved_fixup_kernel(int mode, const int32_t* __restrict__ el, in
                                     const double* __restrict__ w, double* __restrict__ out, StageParams sp) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 2 * n) return;
+  if (mode == MODE_STAGE && stage_stopped(sp)) return;   // converged Richardson iteration
   const int slot = i >> 1, comp = i & 1, nb = 2 * nbs;
   const size_t T = (size_t)el[slot];
   const double* Mi = minv + (size_t)slot * nbs * nbs;
@@ -715,12 +783,15 @@ int hdgc_destroy(hdgc_ctx* c) {
   if (!c) return HDGC_OK;
   cudaFree(c->d_tab); cudaFree(c->d_code); cudaFree(c->d_piola); cudaFree(c->d_minv);
   cudaFree(c->d_sign); cudaFree(c->d_scratch); cudaFree(c->d_scratch2); cudaFree(c->d_modal); cudaFree(c->d_prep); cudaFree(c->d_ftab); cudaFree(c->d_afrag); cudaFree(c->d_mprep); cudaFree(c->d_hu); cudaFree(c->d_hw); cudaFree(c->d_hr); cudaFree(c->d_hin);
-  cudaFree(c->d_uext); cudaFree(c->d_rn); cudaFree(c->d_sum);
+  cudaFree(c->d_uext); cudaFree(c->d_rn); cudaFree(c->d_rpart); cudaFree(c->d_fpart); cudaFree(c->d_ctl); cudaFree(c->d_norms);
+  if (c->h_ctl) cudaFreeHost(c->h_ctl);
+  for (int i = 0; i < 2; ++i) if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  for (auto& g : c->graphs) if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   cudaFree(c->d_dof); cudaFree(c->d_dfac); cudaFree(c->d_inv); cudaFree(c->d_invf); cudaFree(c->d_gl); cudaFree(c->d_rw);
   cudaFree(c->d_celems); cudaFree(c->d_cminv); cudaFree(c->d_citrans); cudaFree(c->d_cpiola); cudaFree(c->d_cres);
   cudaFree(c->d_flag);
   if (c->h_flag) cudaFreeHost(c->h_flag);
-  if (c->h_sum) cudaFreeHost(c->h_sum);
   if (c->blas) cublasDestroy(static_cast<cublasHandle_t>(c->blas));
   delete c;
   return HDGC_OK;
@@ -760,13 +831,9 @@ int hdgc_apply_w(hdgc_ctx* c, const double* u, const double* inflow, double* r_w
   return transfer(c, 1, c->d_scratch2, r_w, st);
 }
 
-int hdgc_substeps(hdgc_ctx* c, const double* u, double* w, const double* inflow, double dt, int32_t nsteps,
-                  void* stream) {
-  if (!c || !u || !w) return hdgc_set_err(HDGC_EINVAL, "null argument");
-  if (nsteps < 0) return hdgc_set_err(HDGC_EINVAL, "nsteps < 0");
-  if (w == u || w == inflow) return hdgc_set_err(HDGC_EINVAL, "w aliases an input");
-  HDGC_ALIGNED(u, w, inflow);
-  cudaStream_t st = (cudaStream_t)stream;
+// the substep batch as a launch sequence on stream st (prep + nsteps update kernels)
+static int substeps_enqueue(hdgc_ctx* c, const double* u, double* w, const double* inflow, double dt, int nsteps,
+                            cudaStream_t st) {
   double* a = w;
   double* b = c->d_scratch;
   if (nsteps > 0 && c->variant >= 1) {
@@ -785,6 +852,88 @@ int hdgc_substeps(hdgc_ctx* c, const double* u, double* w, const double* inflow,
   }
   if (a != w) CUDA_TRY(cudaMemcpyAsync(w, a, sizeof(double) * (size_t)c->nt * c->nb, cudaMemcpyDeviceToDevice, st));
   return HDGC_OK;
+}
+
+// Substep batches run as CUDA graphs: the launch sequence is captured once
+// per (u, w, inflow, dt, nsteps) on a context-owned stream (the PDL launches
+// become programmatic edges) and replayed with one cudaGraphLaunch on the
+// caller's stream, so the host pays one launch per batch instead of nsteps+1.
+// Small LRU cache; HDGC_GRAPHS=0 enqueues the kernels one by one instead.
+static bool graphs_enabled() {
+  // default off: measured with the captured programmatic edges (port 1 or 2) the
+  // batch runs without the PDL overlap (cfg2 k=4: 67 vs 59.5 us per substep; k=1:
+  // 11-12 vs 7.6 us), so stream launches win; HDGC_GRAPHS=1 opts in
+  static const bool on = [] { const char* e = getenv("HDGC_GRAPHS"); return e && e[0] == '1'; }();
+  return on;
+}
+
+static int substeps_graph(hdgc_ctx* c, const double* u, double* w, const double* inflow, double dt, int nsteps,
+                          cudaStream_t st) {
+  uint64_t dtb;
+  memcpy(&dtb, &dt, sizeof(dtb));
+  hdgc_graph* hit = nullptr;
+  for (auto& g : c->graphs)
+    if (g.exec && g.u == u && g.w == w && g.inflow == inflow && g.dt_bits == dtb && g.nsteps == nsteps) hit = &g;
+  if (!hit) {
+    if (!c->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = substeps_enqueue(c, u, w, inflow, dt, nsteps, c->cap_stream);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(c->cap_stream, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (ec != cudaSuccess) return hdgc_set_err(HDGC_ECUDA, "substep graph capture: %s", cudaGetErrorString(ec));
+    if (const char* pe = getenv("HDGC_GRAPH_PORT")) {
+      // development: rewrite the programmatic edges' port (1 = programmatic trigger, 2 = launch completion)
+      size_t ne = 0;
+      cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &ne);
+      std::vector<cudaGraphNode_t> from(ne), to(ne);
+      std::vector<cudaGraphEdgeData> ed(ne);
+      cudaGraphGetEdges_v2(graph, from.data(), to.data(), ed.data(), &ne);
+      for (size_t i = 0; i < ne; ++i) {
+        if (ed[i].type != cudaGraphDependencyTypeProgrammatic) continue;
+        cudaGraphRemoveDependencies_v2(graph, &from[i], &to[i], &ed[i], 1);
+        cudaGraphEdgeData e2 = ed[i];
+        e2.from_port = (unsigned char)atoi(pe);
+        cudaGraphAddDependencies_v2(graph, &from[i], &to[i], &e2, 1);
+      }
+    }
+    if (getenv("HDGC_GRAPH_DEBUG")) {
+      size_t ne = 0;
+      cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &ne);
+      std::vector<cudaGraphNode_t> from(ne), to(ne);
+      std::vector<cudaGraphEdgeData> ed(ne);
+      cudaGraphGetEdges_v2(graph, from.data(), to.data(), ed.data(), &ne);
+      int prog = 0;
+      for (auto& e : ed) prog += e.type == cudaGraphDependencyTypeProgrammatic;
+      fprintf(stderr, "[hdgc] substep graph: %zu edges, %d programmatic (from_port %d)\n", ne, prog,
+              ne ? (int)ed[ne - 1].from_port : -1);
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) return hdgc_set_err(HDGC_ECUDA, "substep graph instantiate: %s", cudaGetErrorString(ei));
+    hit = &c->graphs[c->graph_next];
+    c->graph_next = (c->graph_next + 1) % HDGC_GRAPH_CACHE;
+    if (hit->exec) cudaGraphExecDestroy(hit->exec);
+    *hit = hdgc_graph{u, w, inflow, dtb, nsteps, exec};
+  }
+  CUDA_TRY(cudaGraphLaunch(hit->exec, st));
+  return HDGC_OK;
+}
+
+int hdgc_substeps(hdgc_ctx* c, const double* u, double* w, const double* inflow, double dt, int32_t nsteps,
+                  void* stream) {
+  if (!c || !u || !w) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  if (nsteps < 0) return hdgc_set_err(HDGC_EINVAL, "nsteps < 0");
+  if (w == u || w == inflow) return hdgc_set_err(HDGC_EINVAL, "w aliases an input");
+  HDGC_ALIGNED(u, w, inflow);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nsteps == 0) return HDGC_OK;
+  if (graphs_enabled()) return substeps_graph(c, u, w, inflow, dt, nsteps, st);
+  return substeps_enqueue(c, u, w, inflow, dt, nsteps, st);
 }
 
 int hdgc_propagate(hdgc_ctx* c, const double* u_prev, const double* u_cur, double t_prev, double t_cur,
@@ -866,39 +1015,82 @@ int hdgc_richardson(hdgc_ctx* c, const double* u, const double* g, const double*
   const size_t n = (size_t)c->nt * c->nb, nr = (size_t)c->nt * c->dim;
   int rc;
   if (!c->d_rn && (rc = hdgc_dev_alloc(c, (void**)&c->d_rn, sizeof(double) * nr))) return rc;
-  if (!c->d_sum && (rc = hdgc_dev_alloc(c, (void**)&c->d_sum, sizeof(double)))) return rc;
-  if (!c->h_sum) CUDA_TRY(cudaMallocHost((void**)&c->h_sum, sizeof(double)));
-  if ((rc = prep_any(c, u, st))) return rc;   // convection frozen over the solve
-  double* a = v;
-  double* b = c->d_scratch;
-  StageParams sp;
-  sp.a = 1.0 - ds; sp.b = ds; sp.c = -ds * tau; sp.tau = tau; sp.x = g; sp.rn = c->d_rn;
-  double r0 = 0.0, rn = 0.0;
-  int it = 0;
-  bool conv = false;
-  for (it = 0; it <= max_iter; ++it) {
-    if ((rc = apply_any(c, MODE_STAGE, u, a, inflow, b, sp, true, st))) return rc;
-    sum_kernel<<<1, 1024, 0, st>>>(c->d_rn, nr, c->d_sum);
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(c->h_sum, c->d_sum, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    rn = sqrt(*c->h_sum);
-    if (!std::isfinite(rn)) {
-      // the residual norm sums every updated row: non-finite = norm blow-up
-      hdgc_check_finite(c, stream);
-      return hdgc_set_err(HDGC_EBLOWUP, "richardson: non-finite residual norm at iteration %d (norm blow-up)", it);
-    }
-    if (it == 0) r0 = rn;
-    if (rn <= rho * r0) { conv = true; break; }
-    if (it == max_iter) break;
-    double* t = a; a = b; b = t;          // a = v_{it+1}
+  if (!c->d_rpart && (rc = hdgc_dev_alloc(c, (void**)&c->d_rpart, sizeof(double) * RED_CTAS))) return rc;
+  if (!c->d_ctl && (rc = hdgc_dev_alloc(c, (void**)&c->d_ctl, sizeof(int) * 4))) return rc;
+  if (c->n_norms < max_iter + 1) {
+    cudaFree(c->d_norms);
+    c->d_norms = nullptr;
+    if ((rc = hdgc_dev_alloc(c, (void**)&c->d_norms, sizeof(double) * (max_iter + 1)))) return rc;
+    c->n_norms = max_iter + 1;
   }
-  if (a != v) CUDA_TRY(cudaMemcpyAsync(v, a, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  if (!c->h_ctl) CUDA_TRY(cudaMallocHost((void**)&c->h_ctl, sizeof(int) * 12));
+  for (int i = 0; i < 2; ++i)
+    if (!c->ev[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
+  // sum-factorised kernels (no curved elements) reduce the residual norm inside
+  // the STAGE kernel (StageParams::rpart, rich_fused_reduce) and launch back to
+  // back with PDL; the others write per-(element, component) sums that
+  // richardson_reduce_kernel reduces
+  const bool fused = c->variant == 1 && c->n_curved == 0;
+  const int nblk = (c->nt + 15) / 16;        // CTAs of the sum-factorised kernels (16 elements each)
+  if (fused && !c->d_fpart && (rc = hdgc_dev_alloc(c, (void**)&c->d_fpart, sizeof(double) * nblk))) return rc;
+  if ((rc = prep_any(c, u, st))) return rc;   // convection frozen over the solve
+  CUDA_TRY(cudaMemsetAsync(c->d_ctl, 0, sizeof(int) * 4, st));
+  double* bufs[2] = {v, c->d_scratch};        // iteration it reads bufs[it & 1], writes bufs[(it + 1) & 1]
+  StageParams sp;
+  sp.a = 1.0 - ds; sp.b = ds; sp.c = -ds * tau; sp.tau = tau; sp.x = g; sp.stop = c->d_ctl;
+  if (fused) sp.rpart = c->d_fpart;
+  else sp.rn = c->d_rn;
+  // No host round trip per iteration: iterations are queued in chunks of CH,
+  // each chunk followed by an async copy of the control block; the host waits
+  // only for the chunk BEFORE the one just queued, so the GPU always has a
+  // chunk of work ahead while the host decides whether to queue more.
+  constexpr int CH = 8;
+  int chunk = 0;
+  for (int it = 0; it <= max_iter; ++it) {
+    // fused: STAGE -> final -> STAGE ... all with PDL (the stop flag is read after griddepcontrol.wait)
+    c->pdl = fused && it > 0;
+    rc = apply_any(c, MODE_STAGE, u, bufs[it & 1], inflow, bufs[(it + 1) & 1], sp, true, st);
+    c->pdl = false;
+    if (rc) return rc;
+    if (fused) {
+      CUDA_TRY(launch_maybe_pdl(richardson_final_kernel, 1, 1024, 0, st, true, (const double*)c->d_fpart, nblk, it,
+                                rho, c->d_norms, c->d_ctl));
+    } else {
+      richardson_reduce_kernel<<<RED_CTAS, RED_THREADS, 0, st>>>(c->d_rn, nr, it, rho, c->d_rpart, c->d_norms,
+                                                                 c->d_ctl);
+      CUDA_TRY(cudaGetLastError());
+    }
+    if ((it + 1) % CH == 0 && it < max_iter) {
+      const int slot = chunk & 1;
+      CUDA_TRY(cudaMemcpyAsync(c->h_ctl + 4 * slot, c->d_ctl, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaEventRecord(c->ev[slot], st));
+      if (chunk > 0) {
+        CUDA_TRY(cudaEventSynchronize(c->ev[slot ^ 1]));
+        if (c->h_ctl[4 * (slot ^ 1)] != 0) break;   // stopped: what is queued after it are no-ops
+      }
+      ++chunk;
+    }
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->h_ctl + 8, c->d_ctl, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  const int* ctl = c->h_ctl + 8;
+  const int it = ctl[0] ? ctl[1] : max_iter;
+  double nrm[2] = {0.0, 0.0};
+  CUDA_TRY(cudaMemcpy(&nrm[0], c->d_norms, sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&nrm[1], c->d_norms + it, sizeof(double), cudaMemcpyDeviceToHost));
   if (iters) *iters = it;
-  if (res0) *res0 = r0;
-  if (res_final) *res_final = rn;
-  if (!conv) return hdgc_set_err(HDGC_ENOCONV, "richardson: ||res|| %.3e > rho ||res_0|| after %d iterations", rn, it);
+  if (res0) *res0 = nrm[0];
+  if (res_final) *res_final = nrm[1];
+  if (ctl[2]) {
+    hdgc_check_finite(c, stream);
+    return hdgc_set_err(HDGC_EBLOWUP, "richardson: non-finite residual norm at iteration %d (norm blow-up)", it);
+  }
+  if (bufs[it & 1] != v) {
+    CUDA_TRY(cudaMemcpyAsync(v, bufs[it & 1], sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  if (!ctl[0])
+    return hdgc_set_err(HDGC_ENOCONV, "richardson: ||res|| %.3e > rho ||res_0|| after %d iterations", nrm[1], it);
   return HDGC_OK;
 }
 

@@ -260,7 +260,7 @@ int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double
         return launch(conv2d_sfm_kernel<K, MODE_APPLY, false>, smem);
       }
     }
-    const int smem = F::SMEM_DOUBLES * (int)sizeof(double);
+    const int smem = F::smem_doubles(mode) * (int)sizeof(double);
     const int blocks = (c->nt + F::EPB - 1) / F::EPB;
     auto launch = [&](auto kern) -> int {
       if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
