@@ -23,8 +23,8 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_obj")
 OUT = os.path.join(HERE, "libhdgconv.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-# cuBLAS for the modal-row DGEMM of the frozen-velocity prep (same CUDA image on the GPU box)
-LIBS = ["-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+# no library dependencies beyond the CUDA runtime (every kernel is in csrc/)
+LIBS = []
 FLAGS = ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 

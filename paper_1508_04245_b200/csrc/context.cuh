@@ -72,7 +72,6 @@ struct hdgc_ctx {
   double* d_invf = nullptr;     // (ndof, 2) factors of d_inv
   double* d_gl = nullptr;       // (NT, nb) gathered u_loc (apply_u)
   double* d_rw = nullptr;       // (NT, nb) r_W (apply_u)
-  void* blas = nullptr;         // cublasHandle_t for the modal GEMM (lazily created)
   // curved elements (hdgc_set_curved): d_minv[T] = -(slot + 1) marks them
   int n_curved = 0;
   int32_t* d_celems = nullptr;  // (n_curved,) element ids, ascending
@@ -89,7 +88,7 @@ struct hdgc_ctx {
 
 int hdgc_dev_alloc(hdgc_ctx* c, void** p, size_t bytes);
 // c->d_modal[T][r] = sum_j M[r][j] u[T][j] for r < nr (M row-major [nr][nb] at
-// c->d_tab + off): one DGEMM over all elements on stream st.
+// c->d_tab + off), all elements, on stream st (modal_rows_kernel).
 int hdgc_modal_gemm(hdgc_ctx* c, const double* u, int nb, int nr, size_t off, cudaStream_t st);
 
 namespace hdgc {

@@ -3,7 +3,7 @@
 //
 // The convecting velocity is frozen over an apply and over a whole substep
 // batch, so everything that depends on u alone is
-// evaluated once per batch (prep_fused2d_kernel, or DGEMM + prep_rows2d_kernel) into a
+// evaluated once per batch (prep_tile2d_kernel, prep_fused2d_kernel, or modal_rows_kernel + prep_rows2d_kernel) into a
 // per-element "prep row":
 //   alpha(p) = w_p (u0 + xi_p u1) / (1 - y_p),   beta(p) = w_p u1,
 //   gamma(p) = w_p div u_hat                      at the n^2 volume points,
@@ -229,7 +229,7 @@ prep_fused2d_kernel(const double* __restrict__ u, int nt, double* __restrict__ p
 }
 
 // ---------------------------------------------------------------------------
-// prep, stage 2 (stage 1 = modal rows u_hat | div u_hat by one DGEMM): one CTA
+// prep, stage 2 (stage 1 = modal rows u_hat | div u_hat, modal_rows_kernel): one CTA
 // per tile of 16 elements, one thread per (element, collapsed row b).  The
 // tile's modal rows are staged in smem; thread (e, b) evaluates the velocity on
 // row b by sum factorisation (H_i = sum_j u_ij B_ij(b), values via A_i(xi_a))

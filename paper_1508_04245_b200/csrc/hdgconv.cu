@@ -11,7 +11,6 @@
 #include <string>
 #include <vector>
 
-#include <cublas_v2.h>
 
 #include "common.cuh"
 #include "context.cuh"
@@ -45,21 +44,29 @@ int hdgc_dev_alloc(hdgc_ctx* c, void** p, size_t bytes) {
   return HDGC_OK;
 }
 
-// Row-major out[T][r] = sum_j M[r][j] u[T][j] is, read column-major, the
-// (nr x nt) product M^T(col) x U(col):  C = op_T(A) B with A = M viewed as
-// (nb x nr, lda nb), B = u as (nb x nt, ldb nb), C = d_modal (ldc nr).
+// Modal velocity rows d_modal[T][r] = sum_j M[r][j] u[T][j], r < nr, with M
+// = [coef ; divm] (PB:357-378): one thread per (element, row), M read through
+// L1 (threads of a warp share rows), u row broadcast.  Used by max_speed and
+// the HDGC_PREP=0 development prep; the hot paths stage this product on the
+// FP64 tensor cores inside the tile preps.
+__global__ void __launch_bounds__(256) modal_rows_kernel(const double* __restrict__ M, int nr, int nb,
+                                                         const double* __restrict__ u, int nt,
+                                                         double* __restrict__ out) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)nt * nr) return;
+  const int T = (int)(gid / nr), r = (int)(gid - (long long)T * nr);
+  const double* mr = M + (size_t)r * nb;
+  const double* x = u + (size_t)T * nb;
+  double a = 0.0;
+#pragma unroll 6
+  for (int j = 0; j < nb; ++j) a = fma(__ldg(mr + j), __ldg(x + j), a);
+  out[gid] = a;
+}
+
 int hdgc_modal_gemm(hdgc_ctx* c, const double* u, int nb, int nr, size_t off, cudaStream_t st) {
-  if (!c->blas) {
-    cublasHandle_t h = nullptr;
-    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return hdgc_set_err(HDGC_ECUDA, "cublasCreate failed");
-    c->blas = h;
-  }
-  cublasHandle_t h = static_cast<cublasHandle_t>(c->blas);
-  if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return hdgc_set_err(HDGC_ECUDA, "cublasSetStream failed");
-  const double one = 1.0, zero = 0.0;
-  const cublasStatus_t s = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, nr, c->nt, nb, &one, c->d_tab + off, nb, u, nb,
-                                       &zero, c->d_modal, nr);
-  if (s != CUBLAS_STATUS_SUCCESS) return hdgc_set_err(HDGC_ECUDA, "cublasDgemm (modal rows) failed: %d", (int)s);
+  const long long work = (long long)c->nt * nr;
+  modal_rows_kernel<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(c->d_tab + off, nr, nb, u, c->nt, c->d_modal);
+  CUDA_TRY(cudaGetLastError());
   return HDGC_OK;
 }
 
@@ -382,7 +389,7 @@ __global__ void curved_transfer_kernel(int dir, const int32_t* __restrict__ el, 
 }
 
 // max |J u_hat / detJ| over the curved elements' volume points (per-point J),
-// from the modal rows (u_hat | div) of launch_maxspeed's DGEMM
+// from the modal rows (u_hat | div) of launch_maxspeed (modal_rows_kernel)
 __global__ void curved_maxspeed_kernel(const int32_t* __restrict__ el, int n, int nbs, int mr, int nqv,
                                        const double* __restrict__ vD, const double* __restrict__ modal,
                                        const double* __restrict__ cpiola, unsigned long long* __restrict__ out) {
@@ -792,7 +799,6 @@ int hdgc_destroy(hdgc_ctx* c) {
   cudaFree(c->d_celems); cudaFree(c->d_cminv); cudaFree(c->d_citrans); cudaFree(c->d_cpiola); cudaFree(c->d_cres);
   cudaFree(c->d_flag);
   if (c->h_flag) cudaFreeHost(c->h_flag);
-  if (c->blas) cublasDestroy(static_cast<cublasHandle_t>(c->blas));
   delete c;
   return HDGC_OK;
 }

@@ -184,9 +184,9 @@ int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
   }
   // Measured per launch at 131072 elements (ncu, cold): k=3 the fused
   // thread-per-element kernel (24 us; tile 39 us); k>=4 the tile kernel with
-  // its DMMA modal stage (k=4 47 us vs fused 84; k=5 87 vs DGEMM 41 + rows 78;
+  // its DMMA modal stage (k=4 47 us vs fused 84; k=5 87 vs the round-1 cuBLAS DGEMM 41 + rows 78;
   // k=6 122 vs 81 + 125; k=7 241 vs 102 + 220; k=8 386 vs 123 + 293).
-  // HDGC_PREP=0 selects the older paths (A/B).
+  // HDGC_PREP=0 selects the older paths (A/B; the modal rows now by modal_rows_kernel).
   if constexpr (K >= 4) {
     static const bool tile = [] {
       const char* e = getenv("HDGC_PREP");

@@ -61,3 +61,11 @@ def test_operator_refuses_without_gpu():
     from paper_1508_04245_b200.forms import ConvectionOperator
     with pytest.raises(RuntimeError, match="CUDA"):
         ConvectionOperator(M.generate_structured((0, 0, 1, 1), 2, 2), 2)
+
+
+def test_library_has_no_cublas_dependency():
+    """Every kernel is in csrc/: the library links no BLAS (only the CUDA runtime)."""
+    import subprocess
+    out = subprocess.run(["readelf", "-d", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    needed = [l for l in out.splitlines() if "NEEDED" in l]
+    assert needed and not any("blas" in l.lower() for l in needed), needed

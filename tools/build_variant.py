@@ -28,7 +28,7 @@ def main(name, *flags):
         objs = list(ex.map(comp, sorted(glob.glob(os.path.join(CSRC, "*.cu")))))
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o",
                            os.path.join(out, "libhdgconv.so"), *objs,
-                           "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"])
+                           ])
     print(os.path.join(out, "libhdgconv.so"))
 
 
