@@ -141,6 +141,35 @@ inline void dmma_a_fragments(const double* M, int nr, int nb, double* out) {
       }
 }
 
+// ---------------------------------------------------------------------------
+// HDGC_DEBUG builds (tools/debug_check.py; compute-sanitizer is not available
+// on the GPU pool): every kernel with dynamic shared memory starts with
+// hdgc_debug_prologue, which (1) poisons the whole dynamic smem with NaN, so a
+// read of smem nobody wrote turns the output non-finite, and (2) delays the
+// CTA and then each warp by a pseudo-random amount, which reshuffles the CTA
+// schedule and skews the warps of a CTA against each other, so a missing
+// barrier / mbarrier / PDL wait shows up as output that differs from the
+// release build.  HDGC_ASSERT bounds-checks neighbour / slot indices (device
+// assert: the kernel traps, the host sees a CUDA error).  Release builds: no-ops.
+#ifdef HDGC_DEBUG
+#include <cassert>
+#define HDGC_ASSERT(x) assert(x)
+__device__ __forceinline__ unsigned hdgc_hash(unsigned x) {
+  x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+  return x;
+}
+__device__ __forceinline__ void hdgc_debug_prologue(double* smem, int n_doubles) {
+  for (int i = threadIdx.x; i < n_doubles; i += blockDim.x) smem[i] = __longlong_as_double(0x7ff8dead0000beefLL);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // before any TMA writes the same smem
+  __syncthreads();
+  __nanosleep(hdgc_hash(blockIdx.x * 2654435761u + 17u) % 4000u);
+  __nanosleep(hdgc_hash(blockIdx.x * 40503u + (threadIdx.x >> 5) * 977u + 3u) % 3000u);
+}
+#else
+#define HDGC_ASSERT(x) ((void)0)
+__device__ __forceinline__ void hdgc_debug_prologue(double*, int) {}
+#endif
+
 // Programmatic dependent launch (PDL) between consecutive update kernels of a
 // substep batch (hdgc_substeps): kernel s+1 is launched with the
 // programmatic-stream-serialisation attribute, so its CTAs start while kernel

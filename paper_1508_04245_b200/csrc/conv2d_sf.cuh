@@ -106,7 +106,7 @@ struct SF {
 #define HDGC_XTILE 1
 #endif
   static constexpr bool XTILE = HDGC_XTILE;
-  static constexpr int smem_doubles(int mode) { return SMEM_DOUBLES + (mode == 3 && XTILE ? EPB * NB : 0); }
+  __host__ __device__ static constexpr int smem_doubles(int mode) { return SMEM_DOUBLES + (mode == 3 && XTILE ? EPB * NB : 0); }
 };
 
 // The constant-bank tables of the order compiled in this translation unit
@@ -358,6 +358,7 @@ prep_tile2d_kernel(const double* __restrict__ tab, const double* __restrict__ af
   extern __shared__ __align__(16) double smp[];
   double* s_u = smp;                   // [KS*4][LD]: u transposed, zero rows j >= NB
   double* s_h = smp + P::KS * 4 * LD;  // [MT*8][LD]: u_hat | div u_hat (rows >= NR unused)
+  hdgc_debug_prologue(smp, P::SMEM);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T0 = blockIdx.x * 32;
   const int nel = min(32, nt - T0);
@@ -715,6 +716,7 @@ conv2d_sf_kernel(SFParams p) {
   const double* C = sf_tab<K>();
 
   double* s_x = sm + F::SM_X;              // STAGE: x tile [EPB][NB]
+  hdgc_debug_prologue(sm, F::smem_doubles(MODE));
   const int T0 = blockIdx.x * EPB;
   const int nel = min(EPB, p.nt - T0);
   double2* s_BT = reinterpret_cast<double2*>(sm + F::SM_BT);
@@ -882,6 +884,7 @@ conv2d_sf_kernel(SFParams p) {
       if (on && code >= 0) {
         const int nbT = code >> 2;
         e2 = code & 3;
+        HDGC_ASSERT(nbT < p.nt && e2 < 3);
         src = (nbT >= T0 && nbT < T0 + nel) ? s_w + (nbT - T0) * NB + c * NBS
               : (ed == halo_edge) ? halo : p.w + (size_t)nbT * NB + c * NBS;
       } else if (on) {

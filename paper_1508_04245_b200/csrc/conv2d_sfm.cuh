@@ -94,6 +94,7 @@ prep_modal2d_kernel(const double* __restrict__ tab, const double* __restrict__ a
   extern __shared__ __align__(16) double smp[];
   double* s_u = smp;                   // [KS*4][LD]: u transposed, zero rows j >= NB
   double* s_h = smp + P::KS * 4 * LD;  // [MT*8][LD]: u_hat | div u_hat
+  hdgc_debug_prologue(smp, P::SMEM);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T0 = blockIdx.x * 32;
   const int nel = min(32, nt - T0);
@@ -217,6 +218,7 @@ conv2d_sfm_kernel(SFParams p) {
   double* s_vpart = sm + LY::SM_VPART;     // [32][NBS]: volume warp 1's partial r
   double* s_fD = sm + LY::SM_FD;           // edge trace maps [3][RSTR]
   constexpr int TILE = MODAL ? S::MTILE : F::PREP_TILE;
+  hdgc_debug_prologue(sm, LY::SMEM_DOUBLES);
 
   const int T0 = blockIdx.x * EPB;
   const int nel = min(EPB, p.nt - T0);

@@ -56,6 +56,7 @@ conv2d_thread_kernel(ElemParams p) {
   // neighbour-side facet traces are indexed by the neighbour's local edge (per
   // lane): from a shared-memory copy instead of divergent constant loads
   extern __shared__ __align__(16) double s_fD[];
+  hdgc_debug_prologue(s_fD, 3 * NF * NBS);
   // (filled here, first read in the facet loop: the barrier sits there, so the
   // table's global latency overlaps the u loads and the volume term)
   for (int i = threadIdx.x; i < 3 * NF * NBS; i += blockDim.x) s_fD[i] = p.tab[D::OFF_FD + i];
@@ -163,6 +164,7 @@ conv2d_thread_kernel(ElemParams p) {
     double* wn = uh;  // reuse registers: u_hat is dead after the volume term
     int e2 = 0;
     if (code >= 0) {
+      HDGC_ASSERT((code >> 2) < p.nt && (code & 3) < 3);
       const double* wg = p.w + (size_t)(code >> 2) * NB;
       e2 = code & 3;
 #pragma unroll

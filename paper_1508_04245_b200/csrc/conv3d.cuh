@@ -225,6 +225,7 @@ prep_tile3d_kernel(const double* __restrict__ tab, const double* __restrict__ af
   extern __shared__ __align__(16) double smq[];
   double* s_u = smq;                    // [KS*4][LD]
   double* s_h = smq + P::KS * 4 * LD;   // [MT*8][LD]
+  hdgc_debug_prologue(smq, P::SMEM);
   __shared__ unsigned s_mask[32];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T0 = blockIdx.x * 32;
@@ -400,6 +401,7 @@ conv3d_kernel(Conv3Params p) {
   double* s_R = sm3;                     // [4][NFD][NBS]
   double* s_wo = sm3 + D::RTAB;          // [NBS][96]
   double* s_wn = s_wo + NBS * 96;        // [NBS][96]
+  hdgc_debug_prologue(sm3, D::SMEM / (int)sizeof(double));
   {
     // trace maps: every load of this thread in flight before the smem stores
     constexpr int TOT = 4 * D::NFD * NBS, LOADS = (TOT + D::THREADS - 1) / D::THREADS;
