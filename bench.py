@@ -50,15 +50,25 @@ def pinned_work(k):
     return flops, 3 * nb * 8 + 16
 
 
+def _latest_profile(pattern):
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", pattern)))
+    return files[-1] if files else None
+
+
 def fp64_peak():
-    """Measured FP64 peak (TFLOP/s) from tools/fp64_peak.cu on this pool
-    (profiles/fp64_peak_r01.json); MEASURED_PEAKS.json has no fp64 entry."""
+    """Measured FP64 peaks (TFLOP/s) from tools/fp64_peak_run.py on this pool
+    (newest profiles/fp64_peak_r*.json, with its clock record); MEASURED_PEAKS.json
+    has no fp64 entry.  Returns (max of DMMA / DFMA, DFMA alone, source)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")) as fh:
+        path = _latest_profile("fp64_peak_r*.json")
+        with open(path) as fh:
             d = json.loads(fh.readline())
-        return max(d["dfma_occ8_tflops"], d["dmma_m8n8k4_tflops"]), "profiles/fp64_peak_r01.json (measured DMMA m8n8k4)"
+        src = f"{os.path.relpath(path, ROOT)} (measured; DMMA m8n8k4 {d['dmma_m8n8k4_tflops']}, " \
+              f"DFMA {d['dfma_occ8_tflops']}, DMMA+DFMA mixed {d.get('mixed_dmma_dfma_tflops')}: one shared pipe)"
+        return max(d["dfma_occ8_tflops"], d["dmma_m8n8k4_tflops"]), d["dfma_occ8_tflops"], src
     except Exception:
-        return 37.2, "nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (fallback)"
+        return 37.2, 37.2, "nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (fallback)"
 
 
 def hbm_peak():
@@ -325,12 +335,13 @@ def main():
     if rank != 0:
         return
     flops, byts = pinned_work(K_ORDER)
-    peak, peak_src = fp64_peak()
+    peak, dfma_peak, peak_src = fp64_peak()
     achieved = NT * flops / k_s / 1e12
     traffic = None     # dram read + write bytes per launch of the substep kernel (ncu --set full)
     measured_flop = None
+    ncu_src = _latest_profile("ncu_substep_k4_r*.json")
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_substep_k4_r01.json")) as fh:
+        with open(ncu_src) as fh:
             nc = json.load(fh)
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         traffic = sum(float(nc[k]["value"]) * scale[nc[k]["unit"]]
@@ -355,8 +366,14 @@ def main():
                      "peak_source": peak_src,
                      "algorithmic": f"pinned F(k=4)={flops} flop/element (SURVEY 8d) x {NT} elements per launch",
                      "ncu_fp64_flop_per_launch": measured_flop,
-                     "ncu_source": "profiles/ncu_substep_k4_r01.json",
-                     "hbm_frac": NT * byts / k_s / 1e9 / hbm, "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src},
+                     "ncu_source": os.path.relpath(ncu_src, ROOT) if ncu_src else None,
+                     "hbm_frac": NT * byts / k_s / 1e9 / hbm, "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src,
+                     # hardware fractions: what the kernel really executes / moves (ncu counters
+                     # per launch) over this run's in-stream launch time
+                     "hw_fp64_frac": (measured_flop / k_s / 1e12 / dfma_peak) if measured_flop else None,
+                     "hw_fp64_peak_tflops": dfma_peak,
+                     "hw_dram_frac": (traffic / k_s / 1e9 / hbm) if traffic else None,
+                     "traffic_over_algorithmic": (traffic / (NT * byts)) if traffic else None},
         "cpu_baseline": cpu,
         "e2e": {"value": world * dofs_per_step / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": int(u.nbytes + w.nbytes + inflow.nbytes),
