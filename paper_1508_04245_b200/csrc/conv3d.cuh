@@ -48,10 +48,22 @@ struct Dims3 {
   // different faces hit disjoint bank pairs (the k=3 stride 200 would alias f, f+2)
   static constexpr int RSTR = (NFD * NBS) | 1;
   static constexpr int RTAB = 4 * RSTR;
-  static constexpr int SMEM = (RTAB + 2 * NBS * 96) * 8;             // + own / neighbour w columns
   static constexpr int EPB = 32;                                     // elements per CTA
   static constexpr int THREADS = 3 * EPB;                            // one warp per component
+  // Volume coefficients alpha | beta | gamma | delta are stored tile-blocked and
+  // grouped by collapsed row (ic, ib): [tile of 32][row][field][ia][32], so one
+  // row of one CTA is a single contiguous VROW * 32 doubles (one bulk copy);
+  // the face slots (>= 4 NQ) keep the point-major SoA layout with row stride
+  // ps = nt rounded up to 32 (they start exactly where the volume region ends).
+  static constexpr int VROW = 4 * N1;                                // doubles per element and row
+  static constexpr int NROW = N1 * N1;
+  static constexpr int RBUF = VROW * EPB;                            // one staged row of a CTA
+  static constexpr int SMEM = (RTAB + 2 * NBS * 96 + 2 * RBUF) * 8;  // + own / neighbour w columns + 2 row buffers
+  __host__ __device__ static constexpr size_t vofs(int T, int q, int field) {
+    return ((((size_t)(T >> 5) * NROW + q / N1) * 4 + field) * N1 + q % N1) * 32 + (T & 31);
+  }
 };
+inline int prep3_stride(int nt) { return (nt + 31) & ~31; }
 
 // sum-factorisation tables (constant bank of the order compiled in this TU):
 // D_ijl(a,b,c) = A_i(a) B_ij(b) C_ijl(c) on the collapsed n^3 rule
@@ -108,6 +120,7 @@ struct Prep3Params {
   const double* __restrict__ sgn;
   double* __restrict__ prep;
   int nt;
+  int ps;    // SoA stride of the face slots (prep3_stride)
 };
 
 template <int K>
@@ -119,7 +132,7 @@ prep3d_kernel(Prep3Params p) {
   if (T >= p.nt) return;
   const double* tab = p.tab;
   const double sg = __ldg(p.sgn + T);
-  const size_t nt = (size_t)p.nt;
+  const size_t nt = (size_t)p.ps;   // face-slot stride
   double x[NB];
 #pragma unroll
   for (int j = 0; j < NB; ++j) x[j] = __ldg(p.u + (size_t)T * NB + j);
@@ -184,10 +197,10 @@ prep3d_kernel(Prep3Params p) {
     // flux-form coefficients in collapsed coordinates (chain rule of the Duffy map):
     // g = alpha w_a + beta w_b + gamma w_c + delta w
     const double* pf = c_sf3d + SF3<K>::C_PF + q * 5;
-    p.prep[(size_t)q * nt + T] = sg * fma(pf[0], a0, pf[1] * (a1 + a2));
-    p.prep[(size_t)(NQ + q) * nt + T] = sg * fma(pf[2], a1, pf[3] * a2);
-    p.prep[(size_t)(2 * NQ + q) * nt + T] = sg * pf[4] * a2;
-    p.prep[(size_t)(3 * NQ + q) * nt + T] = sg * pf[4] * dq;
+    p.prep[D::vofs(T, q, 0)] = sg * fma(pf[0], a0, pf[1] * (a1 + a2));
+    p.prep[D::vofs(T, q, 1)] = sg * fma(pf[2], a1, pf[3] * a2);
+    p.prep[D::vofs(T, q, 2)] = sg * pf[4] * a2;
+    p.prep[D::vofs(T, q, 3)] = sg * pf[4] * dq;
   }
 }
 
@@ -216,7 +229,7 @@ struct Prep3Mma {
 template <int K>
 __global__ void __launch_bounds__(32 * Prep3Mma<K>::WARPS)
 prep_tile3d_kernel(const double* __restrict__ tab, const double* __restrict__ afrag, const double* __restrict__ u,
-                   const double* __restrict__ sgn, int nt, double* __restrict__ prep) {
+                   const double* __restrict__ sgn, int nt, int ps, double* __restrict__ prep) {
   using D = Dims3<K>;
   using S = SF3<K>;
   using P = Prep3Mma<K>;
@@ -261,7 +274,7 @@ prep_tile3d_kernel(const double* __restrict__ tab, const double* __restrict__ af
   const bool active = lane < nel;
   const int T = T0 + (active ? lane : 0);
   const double sg = __ldg(sgn + T);
-  const size_t nts = (size_t)nt;
+  const size_t nts = (size_t)ps;   // face-slot stride
   if (warp < 4) {
     // ---- face f = warp: inflow weights, bitmask, inflow matrix
     const int f = warp;
@@ -361,10 +374,10 @@ prep_tile3d_kernel(const double* __restrict__ tab, const double* __restrict__ af
       }
       const int q = (ic * N + ib) * N + ia;
       const double* pf = Cs + S::C_PF + q * 5;
-      prep[(size_t)q * nts + T] = sg * fma(pf[0], a0, pf[1] * (a1 + a2));
-      prep[(size_t)(NQ + q) * nts + T] = sg * fma(pf[2], a1, pf[3] * a2);
-      prep[(size_t)(2 * NQ + q) * nts + T] = sg * pf[4] * a2;
-      prep[(size_t)(3 * NQ + q) * nts + T] = sg * pf[4] * dq;
+      prep[D::vofs(T, q, 0)] = sg * fma(pf[0], a0, pf[1] * (a1 + a2));
+      prep[D::vofs(T, q, 1)] = sg * fma(pf[2], a1, pf[3] * a2);
+      prep[D::vofs(T, q, 2)] = sg * pf[4] * a2;
+      prep[D::vofs(T, q, 3)] = sg * pf[4] * dq;
     }
   }
 }
@@ -380,6 +393,7 @@ struct Conv3Params {
   double* __restrict__ out;
   StageParams st;
   int nt;
+  int ps;    // SoA stride of the face slots (prep3_stride)
 };
 
 // one thread per (element, component); warp w of the CTA = component w of 32
@@ -395,13 +409,32 @@ conv3d_kernel(Conv3Params p) {
   const bool active = T0 < p.nt;
   const int T = active ? T0 : p.nt - 1;
   const double* tab = p.tab;
-  const size_t nt = (size_t)p.nt;
+  const size_t nt = (size_t)p.ps;   // SoA stride of the face slots
   // smem: face trace maps R[4][NFD][NBS] and per-thread w_c / neighbour columns
   extern __shared__ __align__(16) double sm3[];
   double* s_R = sm3;                     // [4][NFD][NBS]
   double* s_wo = sm3 + D::RTAB;          // [NBS][96]
   double* s_wn = s_wo + NBS * 96;        // [NBS][96]
+  double* s_rb = s_wn + NBS * 96;        // [2][VROW][32]: staged volume rows (double buffer)
+  __shared__ __align__(8) uint64_t rbar[2];
   hdgc_debug_prologue(sm3, D::SMEM / (int)sizeof(double));
+  // The volume coefficients of the CTA's 32 elements arrive row by row by TMA
+  // bulk copy (one contiguous VROW x 32 block per collapsed row), two rows in
+  // flight: the three component warps share one copy instead of each issuing
+  // 4 n loads per row, and the loads of row r+2 overlap the work on row r.
+  // They do not depend on the previous kernel, so rows 0 and 1 go before
+  // griddepcontrol.wait.
+  const double* vtile = p.prep + (size_t)(blockIdx.x) * D::NROW * D::RBUF;
+  if (threadIdx.x == 0) {
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    fence_mbar_init();
+#pragma unroll
+    for (int r = 0; r < 2 && r < D::NROW; ++r) {
+      mbar_arrive_expect_tx(&rbar[r], (uint32_t)(D::RBUF * sizeof(double)));
+      bulk_g2s(s_rb + r * D::RBUF, vtile + (size_t)r * D::RBUF, (uint32_t)(D::RBUF * sizeof(double)), &rbar[r]);
+    }
+  }
   {
     // trace maps: every load of this thread in flight before the smem stores
     constexpr int TOT = 4 * D::NFD * NBS, LOADS = (TOT + D::THREADS - 1) / D::THREADS;
@@ -468,16 +501,19 @@ conv3d_kernel(Conv3Params p) {
       for (int ib = 0; ib < N; ++ib) {
         const double* Bb = Cs + S::C_B + ib * NPAIR;
         const double* Bbd = Cs + S::C_BD + ib * NPAIR;
-        const size_t q0 = (size_t)(ic * N + ib) * N;
-        // the row's flux-form coefficients, all issued before the H contraction
+        // the row's flux-form coefficients from the staged row buffer
+        const int row = ic * N + ib;
+        mbar_wait(&rbar[row & 1], (row >> 1) & 1);
+        const double* rb = s_rb + (row & 1) * D::RBUF + (threadIdx.x & 31);
         double pal[N], pbe[N], pga[N], pde[N];
 #pragma unroll
         for (int ia = 0; ia < N; ++ia) {
-          pal[ia] = __ldg(p.prep + (q0 + ia) * nt + T);
-          pbe[ia] = __ldg(p.prep + (NQ + q0 + ia) * nt + T);
-          pga[ia] = __ldg(p.prep + (2 * NQ + q0 + ia) * nt + T);
-          pde[ia] = __ldg(p.prep + (3 * NQ + q0 + ia) * nt + T);
+          pal[ia] = rb[(0 * N + ia) * 32];
+          pbe[ia] = rb[(1 * N + ia) * 32];
+          pga[ia] = rb[(2 * N + ia) * 32];
+          pde[ia] = rb[(3 * N + ia) * 32];
         }
+
         double H[NE], Hb[NE], Hc[NE], K1[NE];
 #pragma unroll
         for (int i = 0; i <= K; ++i) {
@@ -510,6 +546,16 @@ conv3d_kernel(Conv3Params p) {
         for (int i = 0; i <= K; ++i)
 #pragma unroll
           for (int j = 0; j <= K - i; ++j) K2[pidx(i, j)] = fma(K1[i], Bb[pidx(i, j)], K2[pidx(i, j)]);
+        // every warp has consumed this row's coefficients (they fed the FMAs
+        // above): refill the buffer with row + 2 (generic-proxy reads ordered
+        // before the async-proxy write by the barrier + proxy fence)
+        __syncthreads();
+        if (threadIdx.x == 0 && row + 2 < D::NROW) {
+          fence_proxy_async();
+          mbar_arrive_expect_tx(&rbar[row & 1], (uint32_t)(D::RBUF * sizeof(double)));
+          bulk_g2s(s_rb + (row & 1) * D::RBUF, vtile + (size_t)(row + 2) * D::RBUF,
+                   (uint32_t)(D::RBUF * sizeof(double)), &rbar[row & 1]);
+        }
       }
 #pragma unroll
       for (int i = 0; i <= K; ++i)

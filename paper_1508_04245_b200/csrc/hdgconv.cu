@@ -618,7 +618,10 @@ static int create3d(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdg
     // the inflow-face mask and the face inflow matrices S_f (Dims3::PREP)
     const size_t nfd = (size_t)(k + 1) * (k + 2) / 2;
     const size_t prep = 4 * (size_t)nqv + 4 * (size_t)nf + 1 + 4 * (nfd * (nfd + 1) / 2);
-    if ((rc = hdgc_dev_alloc(c, (void**)&c->d_prep, NT * prep * sizeof(double)))) return fail(rc);
+    // (the volume region is tile-blocked by 32 elements: stride prep3_stride(NT))
+    const size_t ps = (size_t)prep3_stride((int)NT);
+    if ((rc = hdgc_dev_alloc(c, (void**)&c->d_prep, ps * prep * sizeof(double)))) return fail(rc);
+    if (cudaMemset(c->d_prep, 0, ps * prep * sizeof(double)) != cudaSuccess) return fail(hdgc_set_err(HDGC_ECUDA, "prep memset"));
   }
 #define SETUP3_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) \
     return fail(hdgc_set_err(HDGC_ECUDA, "%s: %s", #x, cudaGetErrorString(e_))); } while (0)

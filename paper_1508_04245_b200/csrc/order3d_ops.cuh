@@ -63,6 +63,7 @@ int launch3_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
   p.sgn = c->d_sign;
   p.prep = c->d_prep;
   p.nt = c->nt;
+  p.ps = prep3_stride(c->nt);
   static const bool tile = [] {
     const char* e = getenv("HDGC_PREP");
     return !(e && e[0] == '0');
@@ -74,7 +75,7 @@ int launch3_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
     if (smem > 48 * 1024)
       CUDA_TRY(cudaFuncSetAttribute(prep_tile3d_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     prep_tile3d_kernel<K><<<grid3_for(c->nt, 32), 32 * P::WARPS, smem, st>>>(c->d_tab, c->d_afrag, u, c->d_sign,
-                                                                            c->nt, c->d_prep);
+                                                                            c->nt, prep3_stride(c->nt), c->d_prep);
   } else {
     prep3d_kernel<K><<<grid3_for(c->nt, 128), 128, 0, st>>>(p);
   }
@@ -96,6 +97,7 @@ int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, d
   p.out = out;
   p.st = sp;
   p.nt = c->nt;
+  p.ps = prep3_stride(c->nt);
   const unsigned blocks = grid3_for(c->nt, Dims3<K>::EPB);
   constexpr int smem = Dims3<K>::SMEM;
   auto launch = [&](auto kern) -> int {
