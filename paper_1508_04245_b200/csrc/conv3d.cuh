@@ -58,7 +58,12 @@ struct Dims3 {
   static constexpr int VROW = 4 * N1;                                // doubles per element and row
   static constexpr int NROW = N1 * N1;
   static constexpr int RBUF = VROW * EPB;                            // one staged row of a CTA
-  static constexpr int SMEM = (RTAB + 2 * NBS * 96 + 2 * RBUF) * 8;  // + own / neighbour w columns + 2 row buffers
+  // staged row buffers: k = 1, 3 a ring of 3 with producer / consumer
+  // mbarriers, k = 2, 4 a double buffer refilled after a CTA barrier (the ring's
+  // bookkeeping costs registers there: cfg5-size k=4 1993 vs 2419 us, k=2 193 vs 214)
+  static constexpr bool RINGMB = K == 1 || K == 3;
+  static constexpr int NRB = RINGMB ? 3 : 2;
+  static constexpr int SMEM = (RTAB + 2 * NBS * 96 + NRB * RBUF) * 8;  // + own / neighbour w columns + row ring
   __host__ __device__ static constexpr size_t vofs(int T, int q, int field) {
     return ((((size_t)(T >> 5) * NROW + q / N1) * 4 + field) * N1 + q % N1) * 32 + (T & 31);
   }
@@ -415,22 +420,29 @@ conv3d_kernel(Conv3Params p) {
   double* s_R = sm3;                     // [4][NFD][NBS]
   double* s_wo = sm3 + D::RTAB;          // [NBS][96]
   double* s_wn = s_wo + NBS * 96;        // [NBS][96]
-  double* s_rb = s_wn + NBS * 96;        // [2][VROW][32]: staged volume rows (double buffer)
-  __shared__ __align__(8) uint64_t rbar[2];
+  double* s_rb = s_wn + NBS * 96;        // [NRB][VROW][32]: staged volume rows (ring)
+  __shared__ __align__(8) uint64_t rbar[D::NRB];   // full: the row has landed (TMA tx count)
+  __shared__ __align__(8) uint64_t ebar[D::NRB];   // empty: all three warps have consumed it
   hdgc_debug_prologue(sm3, D::SMEM / (int)sizeof(double));
   // The volume coefficients of the CTA's 32 elements arrive row by row by TMA
-  // bulk copy (one contiguous VROW x 32 block per collapsed row), two rows in
-  // flight: the three component warps share one copy instead of each issuing
-  // 4 n loads per row, and the loads of row r+2 overlap the work on row r.
-  // They do not depend on the previous kernel, so rows 0 and 1 go before
-  // griddepcontrol.wait.
+  // bulk copy (one contiguous VROW x 32 block per collapsed row) into a ring of
+  // NRB buffers: the three component warps share one copy instead of each
+  // issuing 4 n loads per row.  Producer / consumer mbarriers: each warp
+  // arrives on the buffer's "empty" barrier once its FMAs have consumed the
+  // row; thread 0 waits for the three arrivals, fences the async proxy (WAR
+  // against the generic-proxy reads) and refills the buffer NRB rows ahead.
+  // Nothing here depends on the previous kernel, so the first NRB rows go
+  // before griddepcontrol.wait.
   const double* vtile = p.prep + (size_t)(blockIdx.x) * D::NROW * D::RBUF;
   if (threadIdx.x == 0) {
-    mbar_init(&rbar[0], 1);
-    mbar_init(&rbar[1], 1);
+#pragma unroll
+    for (int b = 0; b < D::NRB; ++b) {
+      mbar_init(&rbar[b], 1);
+      if (D::RINGMB) mbar_init(&ebar[b], 3);
+    }
     fence_mbar_init();
 #pragma unroll
-    for (int r = 0; r < 2 && r < D::NROW; ++r) {
+    for (int r = 0; r < D::NRB && r < D::NROW; ++r) {
       mbar_arrive_expect_tx(&rbar[r], (uint32_t)(D::RBUF * sizeof(double)));
       bulk_g2s(s_rb + r * D::RBUF, vtile + (size_t)r * D::RBUF, (uint32_t)(D::RBUF * sizeof(double)), &rbar[r]);
     }
@@ -503,8 +515,10 @@ conv3d_kernel(Conv3Params p) {
         const double* Bbd = Cs + S::C_BD + ib * NPAIR;
         // the row's flux-form coefficients from the staged row buffer
         const int row = ic * N + ib;
-        mbar_wait(&rbar[row & 1], (row >> 1) & 1);
-        const double* rb = s_rb + (row & 1) * D::RBUF + (threadIdx.x & 31);
+        const int rbuf = row % D::NRB;
+        const uint32_t rpar = (uint32_t)(row / D::NRB) & 1u;
+        mbar_wait(&rbar[rbuf], rpar);
+        const double* rb = s_rb + rbuf * D::RBUF + (threadIdx.x & 31);
         double pal[N], pbe[N], pga[N], pde[N];
 #pragma unroll
         for (int ia = 0; ia < N; ++ia) {
@@ -546,15 +560,26 @@ conv3d_kernel(Conv3Params p) {
         for (int i = 0; i <= K; ++i)
 #pragma unroll
           for (int j = 0; j <= K - i; ++j) K2[pidx(i, j)] = fma(K1[i], Bb[pidx(i, j)], K2[pidx(i, j)]);
-        // every warp has consumed this row's coefficients (they fed the FMAs
-        // above): refill the buffer with row + 2 (generic-proxy reads ordered
-        // before the async-proxy write by the barrier + proxy fence)
-        __syncthreads();
-        if (threadIdx.x == 0 && row + 2 < D::NROW) {
-          fence_proxy_async();
-          mbar_arrive_expect_tx(&rbar[row & 1], (uint32_t)(D::RBUF * sizeof(double)));
-          bulk_g2s(s_rb + (row & 1) * D::RBUF, vtile + (size_t)(row + 2) * D::RBUF,
-                   (uint32_t)(D::RBUF * sizeof(double)), &rbar[row & 1]);
+        // this warp has consumed the row's coefficients (they fed the FMAs above)
+        if constexpr (D::RINGMB) {
+          __syncwarp();
+          if ((threadIdx.x & 31) == 0) mbar_arrive(&ebar[rbuf]);
+          if (threadIdx.x == 0 && row + D::NRB < D::NROW) {
+            mbar_wait(&ebar[rbuf], rpar);   // all three warps done with the buffer
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&rbar[rbuf], (uint32_t)(D::RBUF * sizeof(double)));
+            bulk_g2s(s_rb + rbuf * D::RBUF, vtile + (size_t)(row + D::NRB) * D::RBUF,
+                     (uint32_t)(D::RBUF * sizeof(double)), &rbar[rbuf]);
+          }
+          __syncwarp();
+        } else {
+          __syncthreads();   // generic-proxy reads of all warps before the async-proxy refill
+          if (threadIdx.x == 0 && row + D::NRB < D::NROW) {
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&rbar[rbuf], (uint32_t)(D::RBUF * sizeof(double)));
+            bulk_g2s(s_rb + rbuf * D::RBUF, vtile + (size_t)(row + D::NRB) * D::RBUF,
+                     (uint32_t)(D::RBUF * sizeof(double)), &rbar[rbuf]);
+          }
         }
       }
 #pragma unroll
