@@ -58,8 +58,8 @@ def run(out):
                 res[f"{tag}_w_{rep}"] = op.apply_w(ud, infd).cpu().numpy()
             op.check_finite()
     os.environ["HDGC_MODAL"] = "0"
-    for k in range(1, 5):
-        m = M3.generate_cube(3)
+    for k, n in ((1, 3), (2, 3), (3, 3), (4, 3), (3, 10), (2, 8)):
+        m = M3.generate_cube(n)
         vp = F3.VectorPotential(3, 5, (0.3, 0.2, -0.5))
         u = F3.interpolate_curl3(m, k, vp)
         w = F3.transfer_I3_host(m, k, u)
@@ -67,8 +67,8 @@ def run(out):
         op = ConvectionOperator(m, k)
         ud, wd, infd = dev(u), dev(w), dev(inf)
         for rep in range(2):
-            res[f"3d{k}_apply_{rep}"] = op.apply(ud, wd, infd).cpu().numpy()
-            res[f"3d{k}_sub_{rep}"] = op.substeps(ud, wd.clone(), 1e-4, 6, infd).cpu().numpy()
+            res[f"3d{k}n{n}_apply_{rep}"] = op.apply(ud, wd, infd).cpu().numpy()
+            res[f"3d{k}n{n}_sub_{rep}"] = op.substeps(ud, wd.clone(), 1e-4, 6, infd).cpu().numpy()
         op.check_finite()
     torch.cuda.synchronize()
     np.savez(out, **res)
