@@ -228,15 +228,7 @@ struct Prep3Mma {
   static constexpr int LD = 40;
   static constexpr int AFRAG = MT * KS * 32;
   static constexpr int WARPS = SF3<K>::N > 4 ? SF3<K>::N : 4;
-  // face inflow matrices as a GEMM per face (k <= 3): S_f[e][j] = sum_q s[e][q] P[q][j],
-  // P[q][j(n,n2)] = D2_n(q) D2_n2(q) (upper triangle j), on the FP64 tensor cores
-  static constexpr bool SFMMA = K <= 3;
-  static constexpr int NF = Dims3<K>::NF, NSYM = Dims3<K>::NSYM;
-  static constexpr int KSF = (NF + 3) / 4, NTF = (NSYM + 7) / 8;
-  static constexpr int BFRAG = SFMMA ? KSF * NTF * 32 : 0;     // B fragments of P, after the A fragments
-  static constexpr int LDSF = 40;                              // row stride of s_s [face][q][element]
-  static constexpr int SMEM_S = SFMMA ? 4 * KSF * 4 * LDSF : 0;
-  static constexpr int SMEM = KS * 4 * LD + MT * 8 * LD + SMEM_S;   // doubles: s_u | s_h | s_s
+  static constexpr int SMEM = KS * 4 * LD + MT * 8 * LD;   // doubles: s_u | s_h
 };
 
 template <int K>
@@ -306,45 +298,7 @@ prep_tile3d_kernel(const double* __restrict__ tab, const double* __restrict__ af
     }
     // the substep kernel reads s and S_f of a face only when its inflow bit is
     // set, so outflow faces write nothing
-    if constexpr (P::SFMMA) {
-      // S_f for the warp's 32 elements at once: (32 x NF) s times (NF x NSYM) P
-      double* s_s = smq + P::KS * 4 * LD + P::MT * 8 * LD + f * P::KSF * 4 * P::LDSF;   // [q][element]
-#pragma unroll
-      for (int q = 0; q < P::KSF * 4; ++q) s_s[q * P::LDSF + lane] = (q < NF && active) ? sv[q] : 0.0;
-      const unsigned inm = __ballot_sync(0xffffffffu, any && active);
-      __syncwarp();
-      if (any && active) {
-        atomicOr(&s_mask[lane], 1u << f);
-#pragma unroll
-        for (int q = 0; q < NF; ++q) prep[(size_t)(4 * NQ + f * NF + q) * nts + T] = sv[q];
-      }
-      if (inm) {
-        const double* bf = afrag + P::AFRAG + lane;
-#pragma unroll 1
-        for (int nt = 0; nt < P::NTF; ++nt) {
-          double d[4][2];
-#pragma unroll
-          for (int mt = 0; mt < 4; ++mt) d[mt][0] = d[mt][1] = 0.0;
-#pragma unroll
-          for (int ks = 0; ks < P::KSF; ++ks) {
-            const double b = __ldg(bf + (ks * P::NTF + nt) * 32);
-#pragma unroll
-            for (int mt = 0; mt < 4; ++mt)
-              dmma_m8n8k4(d[mt][0], d[mt][1], s_s[(ks * 4 + (lane & 3)) * P::LDSF + mt * 8 + (lane >> 2)], b);
-          }
-#pragma unroll
-          for (int mt = 0; mt < 4; ++mt) {
-            const int e = mt * 8 + (lane >> 2);
-            if (!((inm >> e) & 1u)) continue;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int j = nt * 8 + 2 * (lane & 3) + h;
-              if (j < D::NSYM) prep[(size_t)(D::P_S + f * D::NSYM + j) * nts + T0 + e] = d[mt][h];
-            }
-          }
-        }
-      }
-    } else if (any && active) {
+    if (any && active) {
       atomicOr(&s_mask[lane], 1u << f);
 #pragma unroll
       for (int q = 0; q < NF; ++q) prep[(size_t)(4 * NQ + f * NF + q) * nts + T] = sv[q];

@@ -44,25 +44,10 @@ int launch3_setup(hdgc_ctx* c, const hdgc_tables_desc* t) {
   {
     // A fragments of prep_tile3d_kernel's DMMA stage: M = [coef ; divm] ((NB + NBS1) x NB)
     using P = Prep3Mma<K>;
-    std::vector<double> M((size_t)P::NR * P::NB), af(P::AFRAG + P::BFRAG, 0.0);
+    std::vector<double> M((size_t)P::NR * P::NB), af(P::AFRAG);
     memcpy(M.data(), t->coef, sizeof(double) * P::NB * P::NB);
     memcpy(M.data() + (size_t)P::NB * P::NB, t->div_modal, sizeof(double) * (P::NR - P::NB) * P::NB);
     dmma_a_fragments(M.data(), P::NR, P::NB, af.data());
-    if constexpr (P::SFMMA) {
-      // B fragments of P[q][j(n, n2)] = D2_n(q) D2_n2(q), j over the upper triangle
-      // (n <= n2, row-major): tile (ks, nt) lane l = P[4 ks + l % 4][8 nt + l / 4]
-      std::vector<double> Pm((size_t)S::NF * P::NSYM);
-      for (int q = 0; q < S::NF; ++q)
-        for (int n = 0, j = 0; n < S::NFD; ++n)
-          for (int n2 = n; n2 < S::NFD; ++n2, ++j)
-            Pm[(size_t)q * P::NSYM + j] = h[S::C_D2 + q * S::NFD + n] * h[S::C_D2 + q * S::NFD + n2];
-      for (int ks = 0; ks < P::KSF; ++ks)
-        for (int nt = 0; nt < P::NTF; ++nt)
-          for (int l = 0; l < 32; ++l) {
-            const int q = 4 * ks + l % 4, j = 8 * nt + l / 4;
-            af[P::AFRAG + (ks * P::NTF + nt) * 32 + l] = (q < S::NF && j < P::NSYM) ? Pm[(size_t)q * P::NSYM + j] : 0.0;
-          }
-    }
     if ((rc = hdgc_dev_alloc(c, (void**)&c->d_afrag, sizeof(double) * af.size()))) return rc;
     CUDA_TRY(cudaMemcpy(c->d_afrag, af.data(), sizeof(double) * af.size(), cudaMemcpyHostToDevice));
   }
