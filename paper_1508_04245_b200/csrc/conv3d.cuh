@@ -234,7 +234,8 @@ struct Prep3Mma {
 template <int K>
 __global__ void __launch_bounds__(32 * Prep3Mma<K>::WARPS)
 prep_tile3d_kernel(const double* __restrict__ tab, const double* __restrict__ afrag, const double* __restrict__ u,
-                   const double* __restrict__ sgn, int nt, int ps, double* __restrict__ prep) {
+                   const double* __restrict__ sgn, const int32_t* __restrict__ code, int nt, int ps,
+                   double* __restrict__ prep) {
   using D = Dims3<K>;
   using S = SF3<K>;
   using P = Prep3Mma<K>;
@@ -297,11 +298,19 @@ prep_tile3d_kernel(const double* __restrict__ tab, const double* __restrict__ af
       any |= F < 0.0;
     }
     // the substep kernel reads s and S_f of a face only when its inflow bit is
-    // set, so outflow faces write nothing
-    if (any && active) {
-      atomicOr(&s_mask[lane], 1u << f);
+    // set; a warp with no inflow element on this face writes nothing, a warp
+    // with some writes every active lane (zeros where there is no inflow): full
+    // 32-B sectors, no read-modify-write of partially written sectors in L2
+    // (which cost 440 MB of DRAM reads per cfg5 prep)
+    if (any && active) atomicOr(&s_mask[lane], 1u << f);
+    if (__any_sync(0xffffffffu, any && active) && active) {
+      // the point weights s_q are only read for boundary faces with exterior
+      // data (interior faces use S_f alone)
+      const bool bnd = __ldg(code + (size_t)T * 4 + f) < 0;
+      if (__any_sync(__activemask(), bnd)) {
 #pragma unroll
-      for (int q = 0; q < NF; ++q) prep[(size_t)(4 * NQ + f * NF + q) * nts + T] = sv[q];
+        for (int q = 0; q < NF; ++q) prep[(size_t)(4 * NQ + f * NF + q) * nts + T] = sv[q];
+      }
       // fully unrolled: every D2 entry is an immediate constant-bank operand (a
       // runtime-indexed version spent 58% of the kernel in LDC/MIO stalls); k=4
       // (120 x 49 terms) would spill, so it keeps runtime n, n2

@@ -75,7 +75,8 @@ int launch3_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
     if (smem > 48 * 1024)
       CUDA_TRY(cudaFuncSetAttribute(prep_tile3d_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     prep_tile3d_kernel<K><<<grid3_for(c->nt, 32), 32 * P::WARPS, smem, st>>>(c->d_tab, c->d_afrag, u, c->d_sign,
-                                                                            c->nt, prep3_stride(c->nt), c->d_prep);
+                                                                            c->d_code, c->nt, prep3_stride(c->nt),
+                                                                            c->d_prep);
   } else {
     prep3d_kernel<K><<<grid3_for(c->nt, 128), 128, 0, st>>>(p);
   }

@@ -73,7 +73,7 @@ def report(cfg, m, k, u, w, inf, nsub, dim, reps, flush, dt):
         fl, by = bench.pinned_work(k)
     else:
         fl, by = pinned3(k)
-    fp64, _ = bench.fp64_peak()
+    fp64, _, _ = bench.fp64_peak()
     hbm, _ = bench.hbm_peak()
     bound = "hbm" if (dim == 2 and k <= 2) else "fp64"
 
