@@ -122,6 +122,14 @@ typedef struct {
  * positive detJ (2D) / nonzero detJ and ascending vertex ids (3D); failures
  * return HDGC_EINVAL with the reason in hdgc_last_error(). */
 int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tables, hdgc_ctx** out);
+
+/* The same from (mesh, dim = mesh->dim, k) alone: the library
+ * carries the reference-element tables of every supported order (2D k = 1..8,
+ * 3D k = 1..4), generated at build time by the package's basis modules
+ * (restating polybasis.py:47-378, bit-identical to the reference's tables) —
+ * a caller without Python needs only the mesh arrays.  HDGC_EUNSUP for other
+ * (dim, k). */
+int hdgc_create_k(const hdgc_mesh_desc* mesh, int32_t k, hdgc_ctx** out);
 int hdgc_destroy(hdgc_ctx* ctx);
 int hdgc_get_info(const hdgc_ctx* ctx, hdgc_info* info);
 

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("HDGC_LIB") or _DEFAULT_PATH
 
 # exported symbols, in include/hdgconv.h order
 SYMBOLS = (
-    "hdgc_create", "hdgc_destroy", "hdgc_get_info", "hdgc_apply_v", "hdgc_apply_w",
+    "hdgc_create", "hdgc_create_k", "hdgc_destroy", "hdgc_get_info", "hdgc_apply_v", "hdgc_apply_w",
     "hdgc_substeps", "hdgc_transfer", "hdgc_mass_inverse", "hdgc_max_speed",
     "hdgc_apply_v_host", "hdgc_substeps_host", "hdgc_propagate", "hdgc_richardson",
     "hdgc_set_dofmap", "hdgc_gather", "hdgc_scatter", "hdgc_apply_u", "hdgc_set_curved",
@@ -79,6 +79,7 @@ def load(path: str = LIB_PATH):
     vp, i32, d = C.c_void_p, C.c_int32, C.c_double
     sig = {
         "hdgc_create": ([C.POINTER(MeshDesc), C.POINTER(TablesDesc), C.POINTER(vp)], C.c_int),
+        "hdgc_create_k": ([C.POINTER(MeshDesc), i32, C.POINTER(vp)], C.c_int),
         "hdgc_destroy": ([vp], C.c_int),
         "hdgc_get_info": ([vp, C.POINTER(Info)], C.c_int),
         "hdgc_apply_v": ([vp, vp, vp, vp, vp, vp], C.c_int),

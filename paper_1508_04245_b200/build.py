@@ -64,15 +64,38 @@ def _compile(src):
     return obj, res.stderr
 
 
+def _tables_object() -> str:
+    """The built-in reference tables of hdgc_create_k: tables_blob.py writes
+    them (same code path as forms.device_tables), an .incbin assembly stub
+    puts them into .rodata of the library."""
+    blob = os.path.join(OBJ, "tables_blob.bin")
+    asm = os.path.join(OBJ, "tables_blob.S")
+    obj = os.path.join(OBJ, "tables_blob.o")
+    deps = [os.path.join(HERE, f) for f in ("tables_blob.py", "basis.py", "basis3d.py", "forms.py")]
+    if _stale(blob, deps):
+        sys.path.insert(0, ROOT)
+        from paper_1508_04245_b200 import tables_blob
+        tables_blob.write_blob(blob + ".tmp")
+        os.replace(blob + ".tmp", blob)
+    if _stale(obj, [blob]):
+        with open(asm, "w") as fh:
+            fh.write("  .section .rodata\n  .balign 16\n  .globl hdgc_tables_blob\n"
+                     "  .type hdgc_tables_blob, @object\nhdgc_tables_blob:\n"
+                     f'  .incbin "{blob}"\n  .globl hdgc_tables_blob_end\nhdgc_tables_blob_end:\n'
+                     '  .section .note.GNU-stack,"",@progbits\n')
+        subprocess.check_call(["gcc", "-c", "-fPIC", "-o", obj, asm])
+    return obj
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     if force:
-        for f in glob.glob(os.path.join(OBJ, "*.o")):
+        for f in glob.glob(os.path.join(OBJ, "*.o")) + glob.glob(os.path.join(OBJ, "tables_blob.*")):
             os.remove(f)
     srcs = units()
     with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
         results = list(ex.map(_compile, srcs))
-    objs = [o for o, _ in results]
+    objs = [o for o, _ in results] + [_tables_object()]
     if _stale(OUT, objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", OUT + ".tmp", *objs, *LIBS]
         res = subprocess.run(cmd, capture_output=True, text=True)

@@ -789,6 +789,42 @@ int hdgc_create(const hdgc_mesh_desc* mesh, const hdgc_tables_desc* tab, hdgc_ct
 #undef SETUP_TRY
 }
 
+// Built-in reference tables (tables_blob.py, assembled into .rodata by build.py)
+extern "C" const unsigned char hdgc_tables_blob[];
+extern "C" const unsigned char hdgc_tables_blob_end[];
+
+int hdgc_create_k(const hdgc_mesh_desc* mesh, int32_t k, hdgc_ctx** out) {
+  if (!mesh || !out) return hdgc_set_err(HDGC_EINVAL, "null argument");
+  *out = nullptr;
+  constexpr int64_t kMagic = 0x314C425443474448LL;   // "HDGCTBL1"
+  constexpr int kFields = 20;                         // tables_blob.FIELDS
+  const int64_t* hdr = reinterpret_cast<const int64_t*>(hdgc_tables_blob);
+  const size_t blob_bytes = (size_t)(hdgc_tables_blob_end - hdgc_tables_blob);
+  if (blob_bytes < 16 || hdr[0] != kMagic) return hdgc_set_err(HDGC_EINVAL, "built-in table blob is missing or corrupt");
+  const int64_t n = hdr[1];
+  const int64_t per = 5 + 2 * kFields;
+  const double* data = reinterpret_cast<const double*>(hdr + 2 + n * per);
+  for (int64_t e = 0; e < n; ++e) {
+    const int64_t* en = hdr + 2 + e * per;
+    if (en[0] != mesh->dim || en[1] != k) continue;
+    hdgc_tables_desc t;
+    memset(&t, 0, sizeof(t));
+    t.k = k;
+    t.nqv = (int32_t)en[2];
+    t.nf = (int32_t)en[3];
+    t.col_n = (int32_t)en[4];
+    const double* f[kFields];
+    for (int i = 0; i < kFields; ++i) f[i] = en[6 + 2 * i] ? data + en[5 + 2 * i] : nullptr;
+    t.coef = f[0]; t.div_modal = f[1]; t.vol_w = f[2]; t.vol_D = f[3]; t.vol_G = f[4];
+    t.fac_w = f[5]; t.fac_L = f[6]; t.fac_D = f[7]; t.fac_len = f[8];
+    t.col_A = f[9]; t.col_Ad = f[10]; t.col_B = f[11]; t.col_Bd = f[12]; t.col_xi = f[13];
+    t.col_wa = f[14]; t.col_wy = f[15]; t.col_inv1my = f[16]; t.col_C = f[17]; t.col_Cd = f[18];
+    t.col_pf = f[19];
+    return hdgc_create(mesh, &t, out);
+  }
+  return hdgc_set_err(HDGC_EUNSUP, "no built-in tables for dim=%d k=%d (2D: k = 1..8, 3D: k = 1..4)", mesh->dim, k);
+}
+
 int hdgc_destroy(hdgc_ctx* c) {
   if (!c) return HDGC_OK;
   cudaFree(c->d_tab); cudaFree(c->d_code); cudaFree(c->d_piola); cudaFree(c->d_minv);

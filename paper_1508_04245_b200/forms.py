@@ -175,7 +175,7 @@ class ConvectionOperator:
     nothing except their outputs.
     """
 
-    def __init__(self, mesh, k: int, weak_mesh: bool = False):
+    def __init__(self, mesh, k: int, weak_mesh: bool = False, builtin_tables: bool = False):
         lib = _lib.load()
         # operator_for's cache holds contexts by weak mesh reference, so the
         # context (and its device memory) is released together with its mesh
@@ -225,7 +225,11 @@ class ConvectionOperator:
             raise RuntimeError("ConvectionOperator needs a CUDA device (no CPU fallback)")
         torch.cuda.init()
         h = C.c_void_p()
-        _lib.check(lib.hdgc_create(C.byref(md), C.byref(td), C.byref(h)), "hdgc_create")
+        if builtin_tables:
+            # the library's own build-time tables (hdgc_create_k): what a non-Python caller uses
+            _lib.check(lib.hdgc_create_k(C.byref(md), C.c_int32(self.k), C.byref(h)), "hdgc_create_k")
+        else:
+            _lib.check(lib.hdgc_create(C.byref(md), C.byref(td), C.byref(h)), "hdgc_create")
         self._h = h
         self._fin = weakref.finalize(self, lib.hdgc_destroy, h)
         info = _lib.Info()

@@ -69,3 +69,30 @@ def test_library_has_no_cublas_dependency():
     out = subprocess.run(["readelf", "-d", _lib.LIB_PATH], capture_output=True, text=True).stdout
     needed = [l for l in out.splitlines() if "NEEDED" in l]
     assert needed and not any("blas" in l.lower() for l in needed), needed
+
+
+def test_builtin_table_blob_matches_python_tables():
+    """hdgc_create_k's tables (build-time blob in the library) are exactly the
+    arrays ConvectionOperator passes to hdgc_create (same basis modules)."""
+    import struct
+    import numpy as np
+    from paper_1508_04245_b200 import build as Bd
+    from paper_1508_04245_b200 import tables_blob as TB
+    raw = open(os.path.join(Bd.OBJ, "tables_blob.bin"), "rb").read()
+    magic, n = struct.unpack_from("<2q", raw, 0)
+    assert magic == TB.MAGIC and n == len(TB.ORDERS)
+    per = 5 + 2 * len(TB.FIELDS)
+    hdr = struct.unpack_from(f"<{n * per}q", raw, 16)
+    data = np.frombuffer(raw, dtype="<f8", offset=16 + 8 * n * per)
+    for e in range(n):
+        dim, k, nqv, nf, col_n = hdr[e * per:e * per + 5]
+        if (dim, k) not in ((2, 2), (2, 4), (3, 3)):
+            continue
+        ref = TB.entry_tables(dim, k)
+        assert (nqv, nf, col_n) == (ref["nqv"], ref["nf"], ref["col_n"])
+        for i, f in enumerate(TB.FIELDS):
+            off, cnt = hdr[e * per + 5 + 2 * i:e * per + 7 + 2 * i]
+            a = ref["arrays"].get(f)
+            assert (cnt == 0) == (a is None), (dim, k, f)
+            if a is not None:
+                assert np.array_equal(data[off:off + cnt], a), (dim, k, f)

@@ -137,3 +137,29 @@ def test_mesh_validation_3d():
     bad = types.SimpleNamespace(vertices=m.vertices, tets=tets, triangles=tets, facet_elems=m.facet_elems,
                                 facet_local=m.facet_local, n_elements=m.n_elements, n_facets=m.n_facets)
     assert "ascending" in _create_error(bad)
+
+
+@pytest.mark.parametrize("dim,k", [(2, 2), (2, 4), (2, 7), (3, 3)])
+def test_create_k_builtin_tables_bitwise(dim, k):
+    """hdgc_create_k(mesh, k) — the library's build-time tables, what a
+    non-Python caller uses — gives bitwise the results of hdgc_create with the
+    tables passed from Python."""
+    if dim == 2:
+        m, u, w = _field(8, k)
+        inf = None
+    else:
+        m = M3.generate_cube(3)
+        vp = F3.VectorPotential(3, 5, (0.3, 0.2, -0.5))
+        u = F3.interpolate_curl3(m, k, vp)
+        w = F3.transfer_I3_host(m, k, u)
+        inf = dev(F3.inflow_values3(m, k, vp))
+    a = ConvectionOperator(m, k)
+    b = ConvectionOperator(m, k, builtin_tables=True)
+    assert torch.equal(a.apply(dev(u), dev(w), inf), b.apply(dev(u), dev(w), inf))
+    assert torch.equal(a.substeps(dev(u), dev(w), 1e-4, 5, inf), b.substeps(dev(u), dev(w), 1e-4, 5, inf))
+
+
+def test_create_k_unsupported_order():
+    m = M.generate_structured((0, 0, 1, 1), 2, 2)
+    with pytest.raises(RuntimeError, match="status -4"):
+        ConvectionOperator(m, 9, builtin_tables=True)

@@ -26,6 +26,10 @@ def main(name, *flags):
 
     with cf.ThreadPoolExecutor(8) as ex:
         objs = list(ex.map(comp, sorted(glob.glob(os.path.join(CSRC, "*.cu")))))
+    sys.path.insert(0, ROOT)
+    from paper_1508_04245_b200 import build as B
+    os.makedirs(B.OBJ, exist_ok=True)
+    objs.append(B._tables_object())   # built-in tables of hdgc_create_k
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o",
                            os.path.join(out, "libhdgconv.so"), *objs,
                            ])
