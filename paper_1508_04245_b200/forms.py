@@ -186,13 +186,9 @@ class ConvectionOperator:
             from . import basis3d as B3
             self.nbs = B3.nbs3_of(k)
             self.nb = 3 * self.nbs
-            tab = device_tables3(k)
         else:
             self.nb = B.nb_of(k)
             self.nbs = B.nbs_of(k)
-            tab = device_tables(k)
-        self.nf = tab["nf"]
-        self.nqv = tab["nqv"]
         keep = []
 
         def arr(x, dt=np.float64):
@@ -205,21 +201,24 @@ class ConvectionOperator:
             n_facets=mesh.n_facets, vertices=arr(mesh.vertices), elements=arr(mesh.triangles, np.int64),
             facet_elems=arr(mesh.facet_elems, np.int64), facet_local=arr(mesh.facet_local, np.int64),
             facet_perm=None)
-        td = _lib.TablesDesc(
-            k=self.k, nqv=self.nqv, nf=self.nf, coef=arr(tab["coef"]), div_modal=arr(tab["div_modal"]),
-            vol_w=arr(tab["vol_w"]), vol_D=arr(tab["vol_D"]), vol_G=arr(tab["vol_G"]),
-            fac_w=arr(tab["fac_w"]), fac_L=arr(tab["fac_L"]), fac_D=arr(tab["fac_D"]),
-            fac_len=arr(tab["fac_len"]))
-        if self.k >= 3 and self.dim == 2:
-            ct = B.collapsed_tables(self.k)
-            td.col_n = ct["n"]
-            for name in ("A", "Ad", "B", "Bd", "xi", "wa", "wy", "inv1my"):
-                setattr(td, "col_" + name, arr(ct[name]))
-        if self.dim == 3:
-            ct = tab["col3"]
-            td.col_n = ct["n"]
-            for name in ("A", "Ad", "B", "Bd", "C", "Cd", "pf"):
-                setattr(td, "col_" + name, arr(ct[name]))
+        td = None
+        if not builtin_tables:
+            tab = device_tables3(k) if self.dim == 3 else device_tables(k)
+            td = _lib.TablesDesc(
+                k=self.k, nqv=tab["nqv"], nf=tab["nf"], coef=arr(tab["coef"]), div_modal=arr(tab["div_modal"]),
+                vol_w=arr(tab["vol_w"]), vol_D=arr(tab["vol_D"]), vol_G=arr(tab["vol_G"]),
+                fac_w=arr(tab["fac_w"]), fac_L=arr(tab["fac_L"]), fac_D=arr(tab["fac_D"]),
+                fac_len=arr(tab["fac_len"]))
+            if self.k >= 3 and self.dim == 2:
+                ct = B.collapsed_tables(self.k)
+                td.col_n = ct["n"]
+                for name in ("A", "Ad", "B", "Bd", "xi", "wa", "wy", "inv1my"):
+                    setattr(td, "col_" + name, arr(ct[name]))
+            if self.dim == 3:
+                ct = tab["col3"]
+                td.col_n = ct["n"]
+                for name in ("A", "Ad", "B", "Bd", "C", "Cd", "pf"):
+                    setattr(td, "col_" + name, arr(ct[name]))
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("ConvectionOperator needs a CUDA device (no CPU fallback)")
@@ -235,6 +234,8 @@ class ConvectionOperator:
         info = _lib.Info()
         _lib.check(lib.hdgc_get_info(h, C.byref(info)), "hdgc_get_info")
         self.info = info
+        self.nf = info.nf
+        self.nqv = info.nqv
         self.n_elements = info.n_elements
         self.n_boundary_facets = info.n_boundary_facets
         self.curved = None
