@@ -155,6 +155,7 @@ template <int K> __device__ __forceinline__ const double* fd_tab() {
 template <int K>
 __global__ void __launch_bounds__(128)
 prep_fused2d_kernel(const double* __restrict__ u, int nt, double* __restrict__ prep) {
+  pdl_trigger();   // the update kernel after a prep may launch now (PDL, SFParams::prep_dep)
   using F = SF<K>;
   constexpr int N = F::N, NE = F::NE, NBS = F::NBS, NB = F::NB, NBS1 = F::NBS1, NF = F::NF;
   constexpr int O_FL = (NB + NBS1) * NB, O_FW = O_FL + NF * NE, O_FLEN = O_FW + NF;
@@ -240,6 +241,7 @@ template <int K>
 __global__ void __launch_bounds__(16 * SF<K>::N)
 prep_rows2d_kernel(const double* __restrict__ tab, const double* __restrict__ u,
                    const double* __restrict__ modal, int nt, double* __restrict__ prep) {
+  pdl_trigger();   // the update kernel after a prep may launch now (PDL, SFParams::prep_dep)
   using D = Dims<K>;
   using F = SF<K>;
   constexpr int N = F::N, NE = F::NE, NBS = F::NBS, NB = F::NB, NBS1 = F::NBS1, NF = F::NF;
@@ -350,6 +352,7 @@ template <int K>
 __global__ void __launch_bounds__(32 * SF<K>::N, K == 4 ? 4 : (K <= 6 ? 3 : 2))
 prep_tile2d_kernel(const double* __restrict__ tab, const double* __restrict__ afrag, const double* __restrict__ u,
                    int nt, double* __restrict__ prep) {
+  pdl_trigger();   // the update kernel after a prep may launch now (PDL, SFParams::prep_dep)
   using D = Dims<K>;
   using F = SF<K>;
   using P = PrepMma<K>;
@@ -455,6 +458,10 @@ struct SFParams {
   double* __restrict__ out;           // (NT, NB)
   StageParams st;
   int nt;
+  // 1: launched (with PDL) right after the frozen-velocity prep, so the prep
+  // tile is the previous kernel's output and w is not: stage w (and the
+  // tables) before griddepcontrol.wait, the prep tile after it
+  int prep_dep;
 };
 
 #ifndef HDGC_A_UNROLL
@@ -681,22 +688,21 @@ conv2d_sf_kernel(SFParams p) {
     const uint32_t bw = (uint32_t)(nel * NB * sizeof(double));
     const uint32_t bt = (uint32_t)(F::TAB_PAD * sizeof(double));
     mbar_arrive_expect_tx(bar, bp + bw + bt + (MODE == MODE_STAGE && F::XTILE ? bw : 0u));
-    if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
+    if (p.prep_dep) {
+      // right after the prep kernel: w is an input, the prep tile the previous grid's output
+      bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
+      bulk_g2s(s_fD, p.ftab, bt, bar);
+      pdl_wait();
+      if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
+    } else {
+      // substep batch: the prep tile is frozen, w is the previous update kernel's output
+      if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
+      bulk_g2s(s_fD, p.ftab, bt, bar);
+      pdl_wait();
+      bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
+    }
     if (MODE == MODE_STAGE && F::XTILE)
       bulk_g2s(s_x, p.st.x + (size_t)T0 * NB, bw, bar);   // x is not the previous kernel's output
-#ifdef HDGC_L2PF
-    // warm L2 with the prep tile of the CTA that will likely follow on this SM
-    {
-      const unsigned nxt = blockIdx.x + HDGC_L2PF;
-      if (nxt < gridDim.x)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p.prep + (size_t)nxt * F::PREP_TILE),
-                     "r"((uint32_t)(F::PREP_TILE * sizeof(double)))
-                     : "memory");
-    }
-#endif
-    bulk_g2s(s_fD, p.ftab, bt, bar);
-    pdl_wait();   // w is the previous update kernel's output (PDL launch in a substep batch)
-    bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
   }
 
   const int warp = threadIdx.x >> 5;

@@ -131,6 +131,7 @@ struct Prep3Params {
 template <int K>
 __global__ void __launch_bounds__(128)
 prep3d_kernel(Prep3Params p) {
+  pdl_trigger();   // the update kernel after a prep may launch now (PDL, Conv3Params::prep_dep)
   using D = Dims3<K>;
   constexpr int NB = D::NB, NBS = D::NBS, NBS1 = D::NBS1, NFD = D::NFD, NQ = D::NQ, NF = D::NF;
   const int T = blockIdx.x * blockDim.x + threadIdx.x;
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(32 * Prep3Mma<K>::WARPS)
 prep_tile3d_kernel(const double* __restrict__ tab, const double* __restrict__ afrag, const double* __restrict__ u,
                    const double* __restrict__ sgn, const int32_t* __restrict__ code, int nt, int ps,
                    double* __restrict__ prep) {
+  pdl_trigger();   // the update kernel after a prep may launch now (PDL, Conv3Params::prep_dep)
   using D = Dims3<K>;
   using S = SF3<K>;
   using P = Prep3Mma<K>;
@@ -408,6 +410,7 @@ struct Conv3Params {
   StageParams st;
   int nt;
   int ps;    // SoA stride of the face slots (prep3_stride)
+  int prep_dep;   // 1: launched (PDL) right after the prep: stage its rows after griddepcontrol.wait
 };
 
 // one thread per (element, component); warp w of the CTA = component w of 32
@@ -443,6 +446,13 @@ conv3d_kernel(Conv3Params p) {
   // Nothing here depends on the previous kernel, so the first NRB rows go
   // before griddepcontrol.wait.
   const double* vtile = p.prep + (size_t)(blockIdx.x) * D::NROW * D::RBUF;
+  auto issue_first_rows = [&]() {
+#pragma unroll
+    for (int r = 0; r < D::NRB && r < D::NROW; ++r) {
+      mbar_arrive_expect_tx(&rbar[r], (uint32_t)(D::RBUF * sizeof(double)));
+      bulk_g2s(s_rb + r * D::RBUF, vtile + (size_t)r * D::RBUF, (uint32_t)(D::RBUF * sizeof(double)), &rbar[r]);
+    }
+  };
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int b = 0; b < D::NRB; ++b) {
@@ -450,11 +460,7 @@ conv3d_kernel(Conv3Params p) {
       if (D::RINGMB) mbar_init(&ebar[b], 3);
     }
     fence_mbar_init();
-#pragma unroll
-    for (int r = 0; r < D::NRB && r < D::NROW; ++r) {
-      mbar_arrive_expect_tx(&rbar[r], (uint32_t)(D::RBUF * sizeof(double)));
-      bulk_g2s(s_rb + r * D::RBUF, vtile + (size_t)r * D::RBUF, (uint32_t)(D::RBUF * sizeof(double)), &rbar[r]);
-    }
+    if (!p.prep_dep) issue_first_rows();
   }
   {
     // trace maps: every load of this thread in flight before the smem stores
@@ -473,6 +479,7 @@ conv3d_kernel(Conv3Params p) {
     }
   }
   pdl_wait();   // w (and x) come from the previous update kernel under PDL (common.cuh)
+  if (p.prep_dep && threadIdx.x == 0) issue_first_rows();   // the rows are the previous (prep) grid's output
   pdl_trigger();
   constexpr bool SR = HDGC_3D_SMEM_R;
   // SR: w_c from smem (s_wo) and the volume accumulators in smem (s_wn doubles as

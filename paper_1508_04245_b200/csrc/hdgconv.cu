@@ -472,17 +472,36 @@ static int apply_any(hdgc_ctx* c, int mode, const double* u, const double* w, co
   int rc = apply_any_(c, mode, u, w, inflow, out, sp, prep_done, st);
   return rc ? rc : curved_fixup(c, mode, w, out, sp, st);
 }
+// The update kernel right after a frozen-velocity prep launches with PDL: it
+// stages w and its tables while the prep drains and reads the prep only after
+// griddepcontrol.wait (SFParams / Conv3Params::prep_dep).  The modal variant
+// (conv2d_sfm.cuh) and curved batches (fix-up kernel) launch normally.
+static bool prep_pdl_ok(const hdgc_ctx* c) { return !c->modal && c->n_curved == 0; }
+static int after_prep(hdgc_ctx* c, int (*launch)(hdgc_ctx*, int, const double*, const double*, double*,
+                                                 const StageParams&, cudaStream_t),
+                      int mode, const double* w, const double* inflow, double* out, const StageParams& sp,
+                      cudaStream_t st) {
+  const bool pdl = prep_pdl_ok(c);
+  c->pdl = pdl;
+  c->prep_dep = pdl;
+  const int rc = launch(c, mode, w, inflow, out, sp, st);
+  c->pdl = false;
+  c->prep_dep = false;
+  return rc;
+}
 static int apply_any_(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
                       const StageParams& sp, bool prep_done, cudaStream_t st) {
   if (c->variant == 2) {
-    int rc = prep_done ? HDGC_OK : prep3(c, u, st);
+    if (prep_done) return main3(c, mode, w, inflow, out, sp, st);
+    int rc = prep3(c, u, st);
     if (rc) return rc;
-    return main3(c, mode, w, inflow, out, sp, st);
+    return after_prep(c, main3, mode, w, inflow, out, sp, st);
   }
   if (c->variant == 1) {
-    int rc = prep_done ? HDGC_OK : prep(c, u, st);
+    if (prep_done) return sfmain(c, mode, w, inflow, out, sp, st);
+    int rc = prep(c, u, st);
     if (rc) return rc;
-    return sfmain(c, mode, w, inflow, out, sp, st);
+    return after_prep(c, sfmain, mode, w, inflow, out, sp, st);
   }
   return elem(c, mode, u, w, inflow, out, sp, st);
 }
@@ -888,10 +907,13 @@ static int substeps_enqueue(hdgc_ctx* c, const double* u, double* w, const doubl
   }
   for (int s = 0; s < nsteps; ++s) {
     // substeps after the first overlap their prologue with the previous
-    // substep's drain (PDL, common.cuh); curved batches interpose the fix-up kernel
-    c->pdl = s > 0 && c->n_curved == 0;
+    // substep's drain (PDL, common.cuh), the first one with the prep's drain;
+    // curved batches interpose the fix-up kernel
+    c->pdl = c->n_curved == 0 && (s > 0 || (c->variant >= 1 && prep_pdl_ok(c)));
+    c->prep_dep = s == 0 && c->pdl;
     int rc = apply_any(c, MODE_SUBSTEP, u, a, inflow, b, dt, true, st);
     c->pdl = false;
+    c->prep_dep = false;
     if (rc) return rc;
     double* t = a; a = b; b = t;
   }

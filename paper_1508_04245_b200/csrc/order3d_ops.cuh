@@ -99,6 +99,7 @@ int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, d
   p.st = sp;
   p.nt = c->nt;
   p.ps = prep3_stride(c->nt);
+  p.prep_dep = c->prep_dep ? 1 : 0;
   const unsigned blocks = grid3_for(c->nt, Dims3<K>::EPB);
   constexpr int smem = Dims3<K>::SMEM;
   auto launch = [&](auto kern) -> int {

@@ -235,6 +235,7 @@ int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double
     p.out = out;
     p.st = sp;
     p.nt = c->nt;
+    p.prep_dep = c->prep_dep ? 1 : 0;
     if constexpr (K <= 6) {
       // three-warp kernel (conv2d_sfm.cuh): modal prep, or (HDGC_SFM3=1) the point prep
       static const bool sfm3 = [] { const char* e = getenv("HDGC_SFM3"); return e && e[0] == '1'; }();
