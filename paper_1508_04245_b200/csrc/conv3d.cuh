@@ -478,9 +478,13 @@ conv3d_kernel(Conv3Params p) {
       if (i < TOT) s_R[f * D::RSTR + (i - f * D::NFD * NBS)] = v[r];
     }
   }
+  // neighbour codes and the inflow-face mask of the face stage, loaded now so
+  // their latency hides behind the volume term (not dependent loads after it)
+  const int4 codes4 = __ldg(reinterpret_cast<const int4*>(p.code) + T);
   pdl_wait();   // w (and x) come from the previous update kernel under PDL (common.cuh)
   if (p.prep_dep && threadIdx.x == 0) issue_first_rows();   // the rows are the previous (prep) grid's output
   pdl_trigger();
+  const double fmask_d = __ldg(p.prep + (size_t)D::P_MASK * nt + T);
   constexpr bool SR = HDGC_3D_SMEM_R;
   // SR: w_c from smem (s_wo) and the volume accumulators in smem (s_wn doubles as
   // s_r until the face loop), so the sum-factorisation state fits in 136 registers
@@ -629,11 +633,12 @@ conv3d_kernel(Conv3Params p) {
     using S = SF3<K>;
     constexpr int NFD = D::NFD;
     const double* D2 = c_sf3d + S::C_D2;
-    unsigned fm = active ? (unsigned)__ldg(p.prep + (size_t)D::P_MASK * nt + T) : 0u;
+    const int codes[4] = {codes4.x, codes4.y, codes4.z, codes4.w};
+    unsigned fm = active ? (unsigned)fmask_d : 0u;
     if (p.inflow == nullptr) {
 #pragma unroll
       for (int f = 0; f < 4; ++f)
-        if (active && __ldg(p.code + (size_t)T * 4 + f) < 0) fm &= ~(1u << f);   // exterior = own trace
+        if (codes[f] < 0) fm &= ~(1u << f);   // exterior = own trace
     }
     const int nmine = __popc(fm);
     const int nmax = __reduce_max_sync(0xffffffffu, (unsigned)nmine);
@@ -642,7 +647,7 @@ conv3d_kernel(Conv3Params p) {
       const bool on = j < nmine;
       const int f = on ? __ffs(fm) - 1 : 0;
       if (on) fm &= fm - 1;
-      const int code = on ? __ldg(p.code + (size_t)T * 4 + f) : -1;
+      const int code = on ? (f == 0 ? codes[0] : f == 1 ? codes[1] : f == 2 ? codes[2] : codes[3]) : -1;
       int f2 = 0;
       const double* infl = nullptr;
       if (code >= 0) {
