@@ -259,3 +259,30 @@ def test_prep_fallback_paths_hdgc_prep_0():
     assert res.returncode == 0, res.stderr[-2000:]
     errs = [float(x) for x in res.stdout.split()]
     assert len(errs) == 5 and max(errs) < APPLY_TOL, errs
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 6, 8])
+def test_ragged_tail_tiles(k):
+    """Element counts that are not a multiple of any tile size (7 x 5 cells =
+    70 triangles; 16-element sf tiles, 32-element prep tiles, 64-thread blocks):
+    apply + an 8-substep PDL batch vs the C port, with inflow data."""
+    m = M.generate_structured((0.0, 0.0, 1.3, 0.7), 7, 5)
+    sf = F.StreamFunction(5, 4, (0.8, -0.5))
+    u = F.interpolate_curl(m, k, sf)
+    w = F.transfer_I_host(m, k, u)
+    inflow = F.inflow_values(m, k, sf)
+    op = ConvectionOperator(m, k)
+    port = P.PortOperator(m, k, threads=2)
+    assert rel(op.apply(dev(u), dev(w), dev(inflow)), port.apply(u, w, inflow)) < APPLY_TOL
+    dt = F.cfl_dt(m.h_min(), k, F.max_speed_host(m, k, u))
+    wd = op.substeps(dev(u), dev(w), dt, 8, dev(inflow))
+    assert rel(wd, port.substeps(u, w, dt, 8, inflow)) < SUBSTEP_TOL
+
+
+def test_zero_substeps_is_identity():
+    m = M.generate_structured((0.0, 0.0, 1.0, 1.0), 4, 4)
+    k = 4
+    u = F.interpolate_curl(m, k, F.StreamFunction(3, 1))
+    w = F.transfer_I_host(m, k, u)
+    op = ConvectionOperator(m, k)
+    assert torch.equal(op.substeps(dev(u), dev(w), 1e-3, 0), dev(w))
