@@ -32,10 +32,19 @@ __constant__ double c_th[Dims<HDGC_ORDER>::TAB];
 __constant__ double c_th[1];
 #endif
 
-template <int K>
-__host__ __device__ constexpr int thread_smem_bytes() { return 3 * Dims<K>::NF * Dims<K>::NBS * 8; }
-
 constexpr int THREAD_BLOCK = 64;   // small blocks: 2048 CTAs at 131k elements fill the SMs in ~2 full waves
+
+#ifndef HDGC_THR_TMA
+#define HDGC_THR_TMA 1   // stage the CTA's u and w rows with TMA bulk copies (0: per-thread global loads)
+#endif
+// smem (doubles): neighbour-side facet traces fD [3][NF][NBS] (padded even) |
+//                 TMA: u tile [64][NB] | w tile [64][NB]
+template <int K>
+__host__ __device__ constexpr int thread_fd_doubles() { return (3 * Dims<K>::NF * Dims<K>::NBS + 1) & ~1; }
+template <int K>
+__host__ __device__ constexpr int thread_smem_bytes() {
+  return (thread_fd_doubles<K>() + (HDGC_THR_TMA ? 2 * THREAD_BLOCK * Dims<K>::NB : 0)) * 8;
+}
 
 template <int K, int MODE>
 __global__ void __launch_bounds__(THREAD_BLOCK, K == 2 ? 8 : 14)   // 128 / 72 registers: 8 / 14 CTAs per SM
@@ -56,26 +65,56 @@ conv2d_thread_kernel(ElemParams p) {
   // neighbour-side facet traces are indexed by the neighbour's local edge (per
   // lane): from a shared-memory copy instead of divergent constant loads
   extern __shared__ __align__(16) double s_fD[];
-  hdgc_debug_prologue(s_fD, 3 * NF * NBS);
+  hdgc_debug_prologue(s_fD, thread_smem_bytes<K>() / 8);
+  const int tb = blockIdx.x * blockDim.x;
+  const int T0 = tb + threadIdx.x;
+  const bool active = T0 < p.nt;
+  const int T = active ? T0 : p.nt - 1;   // tail lanes recompute the last element, write nothing
+  const int nel = min((int)blockDim.x, p.nt - tb);
+  // TMA: the CTA's u rows and (after griddepcontrol.wait) w rows arrive as two
+  // bulk copies; each thread then reads its own row from smem, and in-tile
+  // neighbours' rows come from smem too
+  double* s_u = s_fD + thread_fd_doubles<K>();
+  double* s_w = s_u + THREAD_BLOCK * NB;
+  __shared__ __align__(8) uint64_t tbar[2];
+  if (HDGC_THR_TMA && threadIdx.x == 0) {
+    mbar_init(&tbar[0], 1);
+    mbar_init(&tbar[1], 1);
+    fence_mbar_init();
+  }
   // (filled here, first read in the facet loop: the barrier sits there, so the
   // table's global latency overlaps the u loads and the volume term)
   for (int i = threadIdx.x; i < 3 * NF * NBS; i += blockDim.x) s_fD[i] = p.tab[D::OFF_FD + i];
-
-  const int T0 = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = T0 < p.nt;
-  const int T = active ? T0 : p.nt - 1;   // tail lanes recompute the last element, write nothing
+  if (HDGC_THR_TMA) {
+    __syncthreads();   // mbarrier init visible
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&tbar[0], (uint32_t)(nel * NB * sizeof(double)));
+      bulk_g2s(s_u, p.u + (size_t)tb * NB, (uint32_t)(nel * NB * sizeof(double)), &tbar[0]);
+    }
+  }
 
   // modal velocity u_hat = coef u and its modal divergence dv = divm u (in P_{k-1})
   double uh[NB];
   double dv[NBS1];
   {
     double u[NB];
-    const double2* ug = reinterpret_cast<const double2*>(p.u + (size_t)T * NB);
+    if (HDGC_THR_TMA) {
+      mbar_wait(&tbar[0], 0);
+      const double2* us = reinterpret_cast<const double2*>(s_u + (T - tb) * NB);
 #pragma unroll
-    for (int j = 0; j < NB / 2; ++j) {
-      const double2 t = __ldg(ug + j);
-      u[2 * j] = t.x;
-      u[2 * j + 1] = t.y;
+      for (int j = 0; j < NB / 2; ++j) {
+        const double2 t = us[j];
+        u[2 * j] = t.x;
+        u[2 * j + 1] = t.y;
+      }
+    } else {
+      const double2* ug = reinterpret_cast<const double2*>(p.u + (size_t)T * NB);
+#pragma unroll
+      for (int j = 0; j < NB / 2; ++j) {
+        const double2 t = __ldg(ug + j);
+        u[2 * j] = t.x;
+        u[2 * j + 1] = t.y;
+      }
     }
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
@@ -97,7 +136,20 @@ conv2d_thread_kernel(ElemParams p) {
   pdl_wait();
   pdl_trigger();
   double w[NB];
-  {
+  if (HDGC_THR_TMA) {
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&tbar[1], (uint32_t)(nel * NB * sizeof(double)));
+      bulk_g2s(s_w, p.w + (size_t)tb * NB, (uint32_t)(nel * NB * sizeof(double)), &tbar[1]);
+    }
+    mbar_wait(&tbar[1], 0);
+    const double2* ws = reinterpret_cast<const double2*>(s_w + (T - tb) * NB);
+#pragma unroll
+    for (int j = 0; j < NB / 2; ++j) {
+      const double2 t = ws[j];
+      w[2 * j] = t.x;
+      w[2 * j + 1] = t.y;
+    }
+  } else {
     const double2* wg = reinterpret_cast<const double2*>(p.w + (size_t)T * NB);
 #pragma unroll
     for (int j = 0; j < NB / 2; ++j) {
@@ -146,7 +198,7 @@ conv2d_thread_kernel(ElemParams p) {
   for (int e = 0; e < 3; ++e) {
     double ue[NE];
 #pragma unroll
-    for (int l = 0; l < NE; ++l) ue[l] = __ldg(p.u + (size_t)T * NB + e * NE + l);
+    for (int l = 0; l < NE; ++l) ue[l] = HDGC_THR_TMA ? s_u[(T - tb) * NB + e * NE + l] : __ldg(p.u + (size_t)T * NB + e * NE + l);
     const double len = flen[e];
     double F[NF];
     bool inflow_edge = false;
@@ -165,10 +217,17 @@ conv2d_thread_kernel(ElemParams p) {
     int e2 = 0;
     if (code >= 0) {
       HDGC_ASSERT((code >> 2) < p.nt && (code & 3) < 3);
-      const double* wg = p.w + (size_t)(code >> 2) * NB;
+      const int nbT = code >> 2;
       e2 = code & 3;
+      if (HDGC_THR_TMA && nbT >= tb && nbT < tb + nel) {
+        const double* ws = s_w + (nbT - tb) * NB;   // in-tile neighbour: its row is staged
 #pragma unroll
-      for (int j = 0; j < NB; ++j) wn[j] = __ldg(wg + j);
+        for (int j = 0; j < NB; ++j) wn[j] = ws[j];
+      } else {
+        const double* wg = p.w + (size_t)nbT * NB;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) wn[j] = __ldg(wg + j);
+      }
     } else if (p.inflow != nullptr) {
       infl = p.inflow + (size_t)(-1 - code) * NF * 2;
     } else {
@@ -209,6 +268,46 @@ conv2d_thread_kernel(ElemParams p) {
   }
 
   // ---- epilogue
+  // APPLY / SUBSTEP with TMA: the rows go back through the w tile and one bulk
+  // store (coalesced), instead of 12 strided 8-byte stores per thread
+  constexpr bool TSTORE = HDGC_THR_TMA && (MODE == MODE_APPLY || MODE == MODE_SUBSTEP);
+  if constexpr (TSTORE) {
+    if (MODE == MODE_SUBSTEP && p.st.cres && active) {
+      const double mflag = __ldg(p.minv + T);
+      if (mflag < 0.0) {
+        double* cr = p.st.cres + (size_t)((int)(-mflag) - 1) * NB;   // curved: raw residual to the fix-up
+#pragma unroll
+        for (int j = 0; j < NB; ++j) cr[j] = r[j];
+      }
+    }
+    double v[NB];
+    if (MODE == MODE_APPLY) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) v[j] = r[j];
+    } else {
+      const double cm = p.st.c * __ldg(p.minv + T);
+      double chk = 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        v[j] = fma(cm, r[j], w[j]);
+        chk += v[j];
+      }
+      guard_finite(p.st.flag, chk);
+    }
+    __syncthreads();   // every thread's facet loop is done reading the w tile
+    if (active) {
+      double2* ws = reinterpret_cast<double2*>(s_w + (T - tb) * NB);
+#pragma unroll
+      for (int j = 0; j < NB / 2; ++j) ws[j] = make_double2(v[2 * j], v[2 * j + 1]);
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_s2g(p.out + (size_t)tb * NB, s_w, (uint32_t)(nel * NB * sizeof(double)));
+      bulk_wait_read();
+    }
+    return;
+  }
   if (!active) return;
   double* og = p.out + (size_t)T * NB;
   if ((MODE == MODE_SUBSTEP || MODE == MODE_STAGE) && p.st.cres) {
