@@ -32,7 +32,10 @@ __constant__ double c_th[Dims<HDGC_ORDER>::TAB];
 __constant__ double c_th[1];
 #endif
 
-constexpr int THREAD_BLOCK = 64;   // small blocks: 2048 CTAs at 131k elements fill the SMs in ~2 full waves
+#ifndef HDGC_THR_BLOCK
+#define HDGC_THR_BLOCK 64
+#endif
+constexpr int THREAD_BLOCK = HDGC_THR_BLOCK;   // small blocks: 2048 CTAs at 131k elements fill the SMs in ~2 full waves
 
 #ifndef HDGC_THR_TMA
 #define HDGC_THR_TMA 1   // stage the CTA's u and w rows with TMA bulk copies (0: per-thread global loads)
@@ -47,7 +50,10 @@ __host__ __device__ constexpr int thread_smem_bytes() {
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(THREAD_BLOCK, K == 2 ? 8 : 14)   // 128 / 72 registers: 8 / 14 CTAs per SM
+#ifndef HDGC_THR_MINB2
+#define HDGC_THR_MINB2 8
+#endif
+__global__ void __launch_bounds__(THREAD_BLOCK, K == 2 ? HDGC_THR_MINB2 * 64 / THREAD_BLOCK : 14 * 64 / THREAD_BLOCK)   // 128 / 72 registers: 8 / 14 CTAs per SM
 conv2d_thread_kernel(ElemParams p) {
   static_assert(K == HDGC_ORDER && K <= 2, "thread variant: k <= 2, tables per translation unit");
   using D = Dims<K>;

@@ -708,6 +708,39 @@ conv3d_kernel(Conv3Params p) {
       }
     }
   }
+  // APPLY / SUBSTEP: the CTA's 32 output rows go through smem (the w columns
+  // are dead after the face stage) and one bulk store, instead of 20 strided
+  // 8-byte stores per thread
+  if constexpr (MODE == MODE_APPLY || MODE == MODE_SUBSTEP) {
+    double v[NBS];
+    if (MODE == MODE_APPLY) {
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) v[m] = r[m];
+    } else {
+      const double cm = p.st.c * __ldg(p.minv + T);
+      double chk = 0.0;
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) {
+        v[m] = fma(cm, r[m], W(m));
+        chk += v[m];
+      }
+      guard_finite(p.st.flag, chk);
+    }
+    __syncthreads();   // every warp is done with s_wo / s_wn
+    const int tb = blockIdx.x * D::EPB, nel = min(D::EPB, p.nt - tb), e = threadIdx.x % D::EPB;
+    double* s_out = s_wo;   // [EPB][NB] row-major (fits in s_wo | s_wn)
+    if (active) {
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) s_out[e * NB + c * NBS + m] = v[m];
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_s2g(p.out + (size_t)tb * NB, s_out, (uint32_t)(nel * NB * sizeof(double)));
+      bulk_wait_read();
+    }
+    return;
+  }
   if (!active) return;
   double* og = p.out + (size_t)T * NB + c * NBS;
   if (MODE == MODE_SUBSTEP) {
