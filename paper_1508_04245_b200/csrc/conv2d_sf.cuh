@@ -66,8 +66,10 @@ struct SF {
 #ifdef HDGC_FACET_ROWS
   static constexpr int FACET_ROWS = HDGC_FACET_ROWS;
 #else
-  // volume rows taken by the facet warp to balance the two warps (measured per k)
-  static constexpr int FACET_ROWS = K == 5 ? 1 : 0;
+  // volume rows taken by the facet warp to balance the two warps (measured per
+  // k at 131k triangles: k=3 0/1 rows 38.1/37.0 us, k=4 2/3 rows 54.3/59.4 us,
+  // k=6 2/3/4 rows 165/176/189 us)
+  static constexpr int FACET_ROWS = K == 3 ? 1 : (K == 4 || K == 6) ? 2 : (K == 5 ? 1 : 0);
 #endif
   static constexpr int PREP_TILE = PREP * 16;      // doubles per tile (EPB = 16)
 #ifdef HDGC_SF_RING
@@ -84,6 +86,13 @@ struct SF {
 #else
   static constexpr bool SMBT = RING;
 #endif
+#ifdef HDGC_W_SMEM
+  static constexpr bool WSMEM = HDGC_W_SMEM;
+#else
+  // volume rows read w_c from the smem tile in every row instead of a register
+  // copy (k=4: 121 registers without spills, 54.3 vs 55.5 us)
+  static constexpr bool WSMEM = K == 4;
+#endif
   static constexpr int RING_SLOT = 3 * N * 16;     // alpha | beta | gamma of one row, [3][N][16]
   // smem (doubles): mbarrier | prep tile [PREP][EPB] or ring [2][3][N][EPB] |
   //                 w tile [EPB][NB] | halo [THREADS][NBS] | fD [3][NF][NBS]
@@ -91,14 +100,29 @@ struct SF {
   static constexpr int SM_PREP = 2;
   static constexpr int SM_W = SM_PREP + (RING ? 2 * RING_SLOT : PREP_TILE);
   static constexpr int SM_HALO = SM_W + EPB * NB;
-  static constexpr int SM_FD = SM_HALO + 32 * NBS + ((32 * NBS) & 1);
+#ifdef HDGC_FV2
+  static constexpr bool FV2 = HDGC_FV2;
+#else
+  // structured-trace facet stage (facets_v2 below).  Measured at 131k triangles
+  // against the per-lane work-list stage it replaces: k=3 37.0 vs 44.0 us, k=4
+  // 54.3 vs 59.4, k=6 165 vs 186; k=5 118.6 vs 105.6 (its 208 registers cost the
+  // fifth CTA per SM), k=7 356 vs 323, k=8 547 vs 458 (ring mode): those keep
+  // the work-list stage.
+  static constexpr bool FV2 = K == 3 || K == 4 || K == 6;
+#endif
+  // per-lane stride of the halo / partial-residual / published-trace rows (odd:
+  // the 32 lanes' rows spread over all banks)
+  static constexpr int HSTR = FV2 ? (((NBS > 3 * NE) ? NBS : 3 * NE) | 1) : NBS;
+  static constexpr int SM_TR = SM_HALO + 32 * HSTR + ((32 * HSTR) & 1);   // FV2: traces [32][HSTR]
+  static constexpr int SM_FD = SM_TR + (FV2 ? 32 * HSTR + ((32 * HSTR) & 1) : 0);
   // smem edge trace maps R[3][NE][NBS], per-edge stride odd (bank spread across lanes)
   static constexpr int RSTR = (NE * NBS) | 1;
   static constexpr int TAB = 3 * NF * NBS;          // constant-bank facet table size (fD)
   static constexpr int TAB_PAD = (3 * RSTR + 1) & ~1; // smem R table, 16-B multiple for the bulk copy
+  static constexpr int TAB_SM = FV2 ? 0 : TAB_PAD;    // FV2 reads the trace maps from the constant bank
   // ring mode: B / B' row tables interleaved [N][NBS](B, B') in smem (uniform LDS.128
   // instead of runtime-indexed constant loads, which ptxas hoists into registers)
-  static constexpr int SM_BT = SM_FD + TAB_PAD;
+  static constexpr int SM_BT = SM_FD + TAB_SM;
   static constexpr int SMEM_DOUBLES = SM_BT + (SMBT ? 2 * N * NBS : 0);
   // STAGE mode adds the x tile [EPB][NB] (bulk-copied with w) after SMEM_DOUBLES
   static constexpr int SM_X = SMEM_DOUBLES;
@@ -118,6 +142,12 @@ struct SF {
 __constant__ double c_sf[SF<HDGC_ORDER>::C_TOTAL];
 __constant__ double c_fd[SF<HDGC_ORDER>::TAB];   // Dubiner traces fD[3][NF][NBS]
 __constant__ double c_fl[SF<HDGC_ORDER>::NF * SF<HDGC_ORDER>::NE];   // Legendre at facet points
+// structured edge trace maps (facets_v2): R_0[i][m(i,j)] (the only non-zeros of
+// edge 0) and R_1[l][m] (zero for l > i + j); R_2[l][m] = (-1)^(i+l) R_1[l][m]
+__constant__ double c_r0[SF<HDGC_ORDER>::NBS];
+__constant__ double c_r1[SF<HDGC_ORDER>::NE * SF<HDGC_ORDER>::NBS];
+// the same non-zeros in order of use (edge_traces / edge_test), read in pairs
+__constant__ __align__(16) double c_tr[(SF<HDGC_ORDER>::NBS + (SF<HDGC_ORDER>::NE) * (SF<HDGC_ORDER>::NE + 1) * (2 * SF<HDGC_ORDER>::NE + 1) / 6 + 1) & ~1];
 // fused prep (k <= 6): [coef ; divm] (NB + NBS1 rows x NB) | fL (NF x NE) | fw (NF) | flen (3)
 #define HDGC_CM_FUSED (HDGC_ORDER <= 4)
 #if HDGC_CM_FUSED
@@ -130,6 +160,9 @@ __constant__ double c_cm[1];
 __constant__ double c_sf[1];
 __constant__ double c_fd[1];
 __constant__ double c_fl[1];
+__constant__ double c_r0[1];
+__constant__ double c_r1[1];
+__constant__ __align__(16) double c_tr[2];
 #define HDGC_CM_FUSED 0
 __constant__ double c_cm[1];
 #endif
@@ -561,11 +594,14 @@ __device__ __forceinline__ void sf_rows(const double* wc, const double* row, dou
   constexpr int b0 = B0, b1 = B1, RU = HDGC_ROW_UNROLL;
   using F = SF<K>;
   constexpr int N = F::N, NBS = F::NBS, EPB = F::EPB;
-  if constexpr (F::RING) {
+  if constexpr (F::RING || F::WSMEM) {
+    // w_c read from the smem tile in every row (no register copy)
 #pragma unroll 1
-    for (int b = b0; b < b1; ++b)
+    for (int b = b0; b < b1; ++b) {
+      if (F::WSMEM) asm volatile("" ::: "memory");   // keep the w loads inside the loop
       sf_row<K>(wc, row + (F::P_AL + b * N) * EPB, row + (F::P_BE + b * N) * EPB, row + (F::P_GA + b * N) * EPB,
                 b, r, sBT);
+    }
   } else {
     double wo[NBS];
 #pragma unroll
@@ -645,6 +681,270 @@ __device__ __forceinline__ double stage_x(const StageParams& st, double mi, doub
   return acc;
 }
 
+// ---------------------------------------------------------------------------
+// Structured edge traces (facets_v2).  The trace of a Dubiner mode
+// D_ij = c_ij (1-y)^i P_i(2 xi - 1) P_j^(2i+1,0)(2y - 1) on a reference edge,
+// expanded in the orthonormal Legendre basis L_l of the edge parameter t:
+//   edge 0 (y = 0, xi = t):      only l = i           -> R_0[i][m]   (NBS values)
+//   edge 1 (xi = 1, y = t):      degree i + j in t    -> R_1[l][m], l <= i + j
+//   edge 2 (xi = 0, y = 1 - t):  P_i(-1) = (-1)^i and L_l(1-t) = (-1)^l L_l(t)
+//                                -> R_2[l][m] = (-1)^(i+l) R_1[l][m]
+// so the traces of one coefficient vector on all three edges cost
+// NBS + sum_d (d+1)^2 FMA with compile-time (immediate constant-bank) operands:
+// E_l / O_l = the even-i / odd-i parts of R_1 w, t1 = E + O, t2 = (-1)^l (E - O).
+// sf_setup checks the three identities on the uploaded tables.
+// The table c_tr holds the non-zeros in the order the unrolled loops below use
+// them: for d = i + j = 0..k, j = 0..d: R_0[i][m], R_1[0..d][m]; it is read in
+// pairs with pinned (asm volatile) constant loads right before their use --
+// left to itself ptxas hoists the ~70 loads of each copy of this code to its
+// top and shuffles them between uniform and vector registers (spills).
+__device__ __forceinline__ double2 ldc_pair(const double* q) {
+  double2 v;
+  asm volatile("ld.const.v2.f64 {%0, %1}, [%2];\n"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(__cvta_generic_to_constant(q)));
+  return v;
+}
+
+template <int K>
+__device__ __forceinline__ void edge_traces(const double (&w)[SF<K>::NBS], double (&t0)[SF<K>::NE],
+                                            double (&t1)[SF<K>::NE], double (&t2)[SF<K>::NE]) {
+  static_assert(K == HDGC_ORDER, "trace tables are per translation unit");
+  constexpr int NE = SF<K>::NE;
+  double E[NE], O[NE];
+#pragma unroll
+  for (int l = 0; l < NE; ++l) t0[l] = E[l] = O[l] = 0.0;
+  int idx = 0;
+  double2 cv = make_double2(0.0, 0.0);
+  auto next = [&]() -> double {
+    if ((idx & 1) == 0) cv = ldc_pair(c_tr + idx);
+    const double v = (idx & 1) ? cv.y : cv.x;
+    ++idx;
+    return v;
+  };
+#pragma unroll
+  for (int d = 0; d <= K; ++d) {
+#pragma unroll
+    for (int j = 0; j <= d; ++j) {
+      const int i = d - j, m = midx(i, j);
+      t0[i] = fma(next(), w[m], t0[i]);
+#pragma unroll
+      for (int l = 0; l <= d; ++l) {
+        if (i & 1) O[l] = fma(next(), w[m], O[l]);
+        else E[l] = fma(next(), w[m], E[l]);
+      }
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < NE; ++l) {
+    t1[l] = E[l] + O[l];
+    t2[l] = (l & 1) ? O[l] - E[l] : E[l] - O[l];
+  }
+}
+
+// r += sum_e R_e^T rho_e with the same structure (transpose of edge_traces)
+template <int K>
+__device__ __forceinline__ void edge_test(const double (&rho0)[SF<K>::NE], const double (&rho1)[SF<K>::NE],
+                                          const double (&rho2)[SF<K>::NE], double (&r)[SF<K>::NBS]) {
+  constexpr int NE = SF<K>::NE;
+  double P[NE], M[NE];   // even-i / odd-i combinations of rho_1 and rho_2
+#pragma unroll
+  for (int l = 0; l < NE; ++l) {
+    const double s2 = (l & 1) ? -rho2[l] : rho2[l];
+    P[l] = rho1[l] + s2;
+    M[l] = rho1[l] - s2;
+  }
+  int idx = 0;
+  double2 cv = make_double2(0.0, 0.0);
+  auto next = [&]() -> double {
+    if ((idx & 1) == 0) cv = ldc_pair(c_tr + idx);
+    const double v = (idx & 1) ? cv.y : cv.x;
+    ++idx;
+    return v;
+  };
+#pragma unroll
+  for (int d = 0; d <= K; ++d) {
+#pragma unroll
+    for (int j = 0; j <= d; ++j) {
+      const int i = d - j, m = midx(i, j);
+      double acc = fma(next(), rho0[i], r[m]);
+#pragma unroll
+      for (int l = 0; l <= d; ++l) acc = fma(next(), (i & 1) ? M[l] : P[l], acc);
+      r[m] = acc;
+    }
+  }
+}
+
+// One halo slot out of line (second and third halo edge of a lane): the
+// neighbour's trace on its edge e2 over the start of the slot.
+template <int K>
+__device__ __noinline__ void halo_trace_slot(double* slot, int e2) {
+  constexpr int NE = SF<K>::NE, NBS = SF<K>::NBS;
+  double nw[NBS];
+#pragma unroll
+  for (int m = 0; m < NBS; ++m) nw[m] = slot[m];
+  double a0[NE], a1[NE], a2[NE];
+  edge_traces<K>(nw, a0, a1, a2);
+#pragma unroll
+  for (int l = 0; l < NE; ++l) slot[l] = e2 == 1 ? a1[l] : (e2 == 2 ? a2[l] : a0[l]);
+}
+
+// More than 32 halo rows in one tile (not on the BASELINE meshes): the
+// neighbour's coefficients straight from global memory, rolled loops, out of line.
+template <int K>
+__device__ __noinline__ void halo_overflow(const double* __restrict__ g, int e2, const double* own, double* dl) {
+  constexpr int NE = SF<K>::NE, NBS = SF<K>::NBS;
+  for (int l = 0; l < NE; ++l) {
+    double t = 0.0;
+    for (int i = 0; i <= K; ++i)
+      for (int j = 0; j <= K - i; ++j) {
+        const int m = midx(i, j);
+        double R = 0.0;
+        if (e2 == 0) R = l == i ? c_r0[m] : 0.0;
+        else if (l <= i + j) R = (e2 == 2 && ((i + l) & 1)) ? -c_r1[l * NBS + m] : c_r1[l * NBS + m];
+        t = fma(R, g[m], t);
+      }
+    dl[l] = ((l & 1) ? -t : t) - own[l];
+  }
+}
+
+// The upwind facet term of one (element, component) lane, all three edges in
+// uniform code.  Own traces on the three edges -> published in s_tr for the
+// in-tile neighbours; out-of-tile neighbours with inflow points get a halo slot
+// (claimed with warp ballots, filled by cp.async while the own traces are
+// computed) and their trace is evaluated here; jump coefficients
+// d_l = (-1)^l t_nbr,l - t_own,l (reversed neighbour parameter, MESH:201), jump at
+// the nf points through L_l(t_q), weighted by the frozen inflow weights s_q,
+// folded back through L and R^T.  No per-lane table reads from shared memory.
+template <int K>
+__device__ __forceinline__ void facets_v2(const SFParams& p, const double* row, const double* wc,
+                                          const int (&codes)[3], double* s_tr, double* s_halo, int T0, int nel,
+                                          int lane, int c, bool active, double (&r)[SF<K>::NBS]) {
+  using F = SF<K>;
+  constexpr int NE = F::NE, NBS = F::NBS, NB = F::NB, NF = F::NF, EPB = F::EPB, HSTR = F::HSTR;
+  const double* FL = fl_tab<K>();
+  unsigned emask = 0, hmask = 0;
+  if (active) {
+#pragma unroll
+    for (int ed = 0; ed < 3; ++ed) {
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < NF; ++q) any |= row[(F::P_S + ed * NF + q) * EPB] != 0.0;
+      const bool has_ext = codes[ed] >= 0 || p.inflow != nullptr;   // else exterior = own trace
+      if (any && has_ext) {
+        emask |= 1u << ed;
+        const int nbT = codes[ed] >> 2;
+        if (codes[ed] >= 0 && (nbT < T0 || nbT >= T0 + nel)) hmask |= 1u << ed;
+      }
+    }
+  }
+  // halo slots: lane-ordered claims per edge; slots >= 32 (rare) read global memory directly
+  int hslot[3];
+  {
+    int off = 0;
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int ed = 0; ed < 3; ++ed) {
+      const bool need = (hmask >> ed) & 1u;
+      const unsigned bal = __ballot_sync(0xffffffffu, need);
+      hslot[ed] = need ? off + __popc(bal & lt) : -1;
+      off += __popc(bal);
+      if (need && hslot[ed] < 32) {
+        const double* g = p.w + (size_t)(codes[ed] >> 2) * NB + c * NBS;
+        double* dst = s_halo + hslot[ed] * HSTR;
+#pragma unroll
+        for (int m = 0; m < NBS; ++m) cp_async8(dst + m, g + m);
+      }
+    }
+  }
+  // halo traces: the neighbour's trace on its edge e2, written back over the
+  // start of the slot (only this lane reads or writes its slots).  First round
+  // in line (every lane runs the same code; lanes without a halo edge discard
+  // the result), further rounds (a lane with two or three out-of-tile inflow
+  // edges: the ends of a tile) out of line.
+  unsigned pend = 0;
+#pragma unroll
+  for (int ed = 0; ed < 3; ++ed)
+    if (hslot[ed] >= 0 && hslot[ed] < 32) pend |= 1u << ed;
+  if (hmask) cp_async_wait_all();
+  if (__any_sync(0xffffffffu, pend != 0)) {
+    const double* src = wc;
+    double* dst = nullptr;
+    int e2 = 0;
+    if (pend) {
+      const int ed = __ffs(pend) - 1;
+      pend &= pend - 1;
+      const int slot = ed == 0 ? hslot[0] : (ed == 1 ? hslot[1] : hslot[2]);
+      const int code = ed == 0 ? codes[0] : (ed == 1 ? codes[1] : codes[2]);
+      HDGC_ASSERT((code >> 2) < p.nt && (code & 3) < 3);
+      dst = s_halo + slot * HSTR;
+      src = dst;
+      e2 = code & 3;
+    }
+    double nw[NBS];
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) nw[m] = src[m];
+    double a0[NE], a1[NE], a2[NE];
+    edge_traces<K>(nw, a0, a1, a2);
+    if (dst != nullptr) {
+#pragma unroll
+      for (int l = 0; l < NE; ++l) dst[l] = e2 == 1 ? a1[l] : (e2 == 2 ? a2[l] : a0[l]);
+    }
+    while (__any_sync(0xffffffffu, pend != 0)) {
+      if (pend) {
+        const int ed = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const int slot = ed == 0 ? hslot[0] : (ed == 1 ? hslot[1] : hslot[2]);
+        const int code = ed == 0 ? codes[0] : (ed == 1 ? codes[1] : codes[2]);
+        halo_trace_slot<K>(s_halo + slot * HSTR, code & 3);
+      }
+    }
+  }
+  asm volatile("bar.sync 2, 64;\n" ::: "memory");   // (T) own traces of the tile published by the volume warp
+  double rho[3][NE];
+#pragma unroll
+  for (int ed = 0; ed < 3; ++ed) {
+    const bool on = (emask >> ed) & 1u;
+    const int code = codes[ed];
+    const double* own = s_tr + lane * HSTR + ed * NE;
+    const double* nsrc = own;     // placeholder when there is no neighbour trace
+    bool has_nb = false;
+    const double* infl = nullptr;
+    if (hslot[ed] >= 0) {
+      nsrc = s_halo + (hslot[ed] & 31) * HSTR;
+      has_nb = hslot[ed] < 32;
+    } else if (on && code >= 0) {
+      HDGC_ASSERT((code >> 2) >= T0 && (code >> 2) < T0 + nel && (code & 3) < 3);
+      nsrc = s_tr + (((code >> 2) - T0) * 2 + c) * HSTR + (code & 3) * NE;
+      has_nb = true;
+    } else if (on) {
+      infl = p.inflow + (size_t)(-1 - code) * NF * 2 + c;
+    }
+    double dl[NE];
+#pragma unroll
+    for (int l = 0; l < NE; ++l) {
+      const double tn = has_nb ? nsrc[l] : 0.0;
+      dl[l] = ((l & 1) ? -tn : tn) - own[l];
+      rho[ed][l] = 0.0;
+    }
+    if (hslot[ed] >= 32) halo_overflow<K>(p.w + (size_t)(code >> 2) * NB + c * NBS, code & 3, own, dl);
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      const double sq = on ? row[(F::P_S + ed * NF + q) * EPB] : 0.0;
+      double J = 0.0;
+#pragma unroll
+      for (int l = 0; l < NE; ++l) J = fma(dl[l], FL[q * NE + l], J);
+      if (infl != nullptr && sq != 0.0) J += __ldg(infl + 2 * q);
+      const double sj = sq * J;
+#pragma unroll
+      for (int l = 0; l < NE; ++l) rho[ed][l] = fma(sj, FL[q * NE + l], rho[ed][l]);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < NBS; ++m) r[m] = 0.0;
+  edge_test<K>(rho[0], rho[1], rho[2], r);
+}
+
 // Two warps per CTA on one tile of EPB = 16 elements: warp 0 computes the
 // volume term, warp 1 the upwind facet term, concurrently; lane l of either
 // warp owns (element l/2, component l%2).  The facet warp leaves its partial
@@ -656,7 +956,7 @@ __device__ __forceinline__ double stage_x(const StageParams& st, double mi, doub
 #else
 // register caps 128 / 256 / 255: k <= 4 runs 8 CTAs/SM at 128 registers (a few
 // spilled bytes; k=4 69.8 -> 66.5 us, k=3 53.2 -> 49.7 us measured); k >= 7: 4 CTAs/SM by smem + regs
-#define HDGC_SF_MINB_OF(K) (K <= 4 ? 8 : (K <= 6 ? 4 : 2))
+#define HDGC_SF_MINB_OF(K) (K == 3 ? 9 : K <= 4 ? 8 : (K <= 6 ? 4 : 2))
 #endif
 template <int K, int MODE>
 __global__ void __launch_bounds__(SF<K>::THREADS, HDGC_SF_MINB_OF(K))
@@ -686,18 +986,18 @@ conv2d_sf_kernel(SFParams p) {
   if (threadIdx.x == 0) {
     const uint32_t bp = F::RING ? 0u : (uint32_t)(F::PREP_TILE * sizeof(double));
     const uint32_t bw = (uint32_t)(nel * NB * sizeof(double));
-    const uint32_t bt = (uint32_t)(F::TAB_PAD * sizeof(double));
+    const uint32_t bt = (uint32_t)(F::TAB_SM * sizeof(double));   // 0 with FV2
     mbar_arrive_expect_tx(bar, bp + bw + bt + (MODE == MODE_STAGE && F::XTILE ? bw : 0u));
     if (p.prep_dep) {
       // right after the prep kernel: w is an input, the prep tile the previous grid's output
       bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
-      bulk_g2s(s_fD, p.ftab, bt, bar);
+      if (!F::FV2) bulk_g2s(s_fD, p.ftab, bt, bar);
       pdl_wait();
       if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
     } else {
       // substep batch: the prep tile is frozen, w is the previous update kernel's output
       if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
-      bulk_g2s(s_fD, p.ftab, bt, bar);
+      if (!F::FV2) bulk_g2s(s_fD, p.ftab, bt, bar);
       pdl_wait();
       bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
     }
@@ -711,13 +1011,15 @@ conv2d_sf_kernel(SFParams p) {
   const int c = lane & 1;
   const bool active = le < nel;
   const int T = T0 + (active ? le : 0);
-  double* part = s_halo + lane * NBS;
+  double* part = s_halo + lane * F::HSTR;
   const double* gtile = p.prep + (size_t)blockIdx.x * F::PREP_TILE;
   // the element's prep column (slot j at row[j * EPB]): smem tile, or (ring) the global tile
   const double* row = (F::RING ? gtile : s_prep) + (active ? le : 0);
   double r[NBS];
+  if (!F::FV2) {
 #pragma unroll
-  for (int m = 0; m < NBS; ++m) r[m] = 0.0;
+    for (int m = 0; m < NBS; ++m) r[m] = 0.0;
+  }
 
   if (warp == 0) {
     // ===================== volume warp =====================
@@ -728,8 +1030,35 @@ conv2d_sf_kernel(SFParams p) {
     mbar_wait(bar, 0);
     if (stopped) return;   // converged Richardson iteration: queued after the stop, writes nothing
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
+    if constexpr (F::FV2) {
+      // own traces on the three edges -> s_tr row of this lane (read by the facet
+      // warp: own side of the jumps, and the in-tile neighbours)
+      double wv[NBS];
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) wv[m] = wc[m];
+      double t0[NE], t1[NE], t2[NE];
+      edge_traces<K>(wv, t0, t1, t2);
+      double* mine = sm + F::SM_TR + lane * F::HSTR;
+#pragma unroll
+      for (int l = 0; l < NE; ++l) {
+        mine[l] = t0[l];
+        mine[NE + l] = t1[l];
+        mine[2 * NE + l] = t2[l];
+      }
+      asm volatile("bar.arrive 2, 64;\n" ::: "memory");   // (T)
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) r[m] = 0.0;   // (not live across the traces)
+    }
     if (F::RING) sf_rows_ring<K>(wc, gtile, s_prep, active ? le : 0, lane, N - F::FACET_ROWS, r, s_BT);
-    else sf_rows<K, 0, N - F::FACET_ROWS>(wc, row, r, s_BT);
+    else {
+#ifdef HDGC_ROW_SPLIT
+      constexpr int NV = N - F::FACET_ROWS, H = HDGC_ROW_SPLIT;
+      sf_rows<K, 0, H>(wc, row, r, s_BT);
+      sf_rows<K, H, NV>(wc, row, r, s_BT);
+#else
+      sf_rows<K, 0, N - F::FACET_ROWS>(wc, row, r, s_BT);
+#endif
+    }
     asm volatile("bar.sync 1, 64;\n" ::: "memory");   // (A) facet partial r ready, in-tile w reads done
     double racc = 0.0;   // STAGE: this lane's residual sum of squares
     if (active) {
@@ -780,6 +1109,9 @@ conv2d_sf_kernel(SFParams p) {
     mbar_wait(bar, 0);
     if (stopped) return;
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
+    if constexpr (F::FV2) {
+      facets_v2<K>(p, row, wc, codes, sm + F::SM_TR, s_halo, T0, nel, lane, c, active, r);
+    } else {
     double* halo = part;
     int halo_edge = -1;
     if (active) {
@@ -881,6 +1213,7 @@ conv2d_sf_kernel(SFParams p) {
         r[m] = acc;
       }
     }
+    }   // !FV2
     // balance: the facet warp also takes the last FACET_ROWS volume rows
     if (F::FACET_ROWS > 0) sf_rows<K, N - F::FACET_ROWS, N>(wc, row, r, s_BT);
     __syncwarp();          // halo reads of all lanes done before the partials overwrite it

@@ -313,6 +313,37 @@ int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& 
                  packed[D::OFF_FL + q * F::NE + l];
           ft[e * F::RSTR + l * F::NBS + m] = a;
         }
+    {
+      // structured trace maps for facets_v2 (conv2d_sf.cuh): R_0 diagonal in i, R_1
+      // lower-triangular in the total degree, R_2 = (-1)^(i+l) R_1 -- checked here
+      std::vector<double> r0(F::NBS, 0.0), r1(F::NE * F::NBS, 0.0);
+      double bad = 0.0;
+      for (int i = 0; i <= K; ++i)
+        for (int j = 0; j <= K - i; ++j) {
+          const int m = midx(i, j);
+          for (int l = 0; l < F::NE; ++l) {
+            const double v0 = ft[0 * F::RSTR + l * F::NBS + m], v1 = ft[1 * F::RSTR + l * F::NBS + m],
+                         v2 = ft[2 * F::RSTR + l * F::NBS + m];
+            if (l == i) r0[m] = v0; else bad = fmax(bad, fabs(v0));
+            if (l <= i + j) r1[l * F::NBS + m] = v1; else bad = fmax(bad, fabs(v1));
+            bad = fmax(bad, fabs(v2 - (((i + l) & 1) ? -v1 : v1)));
+          }
+        }
+      if (bad > 1e-12)
+        return hdgc_set_err(HDGC_EINVAL, "facet tables do not have the Dubiner edge-trace structure (defect %.3e)", bad);
+      CUDA_TRY(cudaMemcpyToSymbol(c_r0, r0.data(), sizeof(double) * F::NBS));
+      CUDA_TRY(cudaMemcpyToSymbol(c_r1, r1.data(), sizeof(double) * F::NE * F::NBS));
+      std::vector<double> tr;   // order of use in edge_traces / edge_test
+      for (int d = 0; d <= K; ++d)
+        for (int j = 0; j <= d; ++j) {
+          const int m = midx(d - j, j);
+          tr.push_back(r0[m]);
+          for (int l = 0; l <= d; ++l) tr.push_back(r1[l * F::NBS + m]);
+        }
+      tr.resize((tr.size() + 1) & ~size_t(1), 0.0);
+      if (tr.size() * sizeof(double) != sizeof(c_tr)) return hdgc_set_err(HDGC_EINVAL, "trace table size");
+      CUDA_TRY(cudaMemcpyToSymbol(c_tr, tr.data(), sizeof(double) * tr.size()));
+    }
 #if HDGC_CM_FUSED
     {
       // [coef ; divm] | fL | fw | flen for the fused prep kernel
