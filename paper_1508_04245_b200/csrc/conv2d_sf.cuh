@@ -537,7 +537,11 @@ __device__ __forceinline__ void sf_row(const WS& wv, const double* al, const dou
   double Kc[NE];
 #pragma unroll
   for (int i = 0; i <= K; ++i) Kc[i] = 0.0;
+#ifdef HDGC_A_UNROLL_SF
+  constexpr int AU = F::RING ? HDGC_A_UNROLL : HDGC_A_UNROLL_SF;
+#else
   constexpr int AU = F::RING ? HDGC_A_UNROLL : 64;
+#endif
 #pragma unroll AU
   for (int a = 0; a < N; ++a) {
     double wv0 = 0.0, wxi = 0.0, wyy = 0.0;
@@ -819,9 +823,10 @@ __device__ __noinline__ void halo_overflow(const double* __restrict__ g, int e2,
 template <int K>
 __device__ __forceinline__ void facets_v2(const SFParams& p, const double* row, const double* wc,
                                           const int (&codes)[3], double* s_tr, double* s_halo, int T0, int nel,
-                                          int lane, int c, bool active, double (&r)[SF<K>::NBS]) {
+                                          int lane, int c, bool active, double (&r)[SF<K>::NBS],
+                                          const double2* sBT) {
   using F = SF<K>;
-  constexpr int NE = F::NE, NBS = F::NBS, NB = F::NB, NF = F::NF, EPB = F::EPB, HSTR = F::HSTR;
+  constexpr int N = F::N, NE = F::NE, NBS = F::NBS, NB = F::NB, NF = F::NF, EPB = F::EPB, HSTR = F::HSTR;
   const double* FL = fl_tab<K>();
   unsigned emask = 0, hmask = 0;
   if (active) {
@@ -857,6 +862,11 @@ __device__ __forceinline__ void facets_v2(const SFParams& p, const double* row, 
       }
     }
   }
+  // balance: the facet warp takes the last FACET_ROWS volume rows, while its halo
+  // rows are in flight
+#pragma unroll
+  for (int m = 0; m < NBS; ++m) r[m] = 0.0;
+  if (F::FACET_ROWS > 0) sf_rows<K, N - F::FACET_ROWS, N>(wc, row, r, sBT);
   // halo traces: the neighbour's trace on its edge e2, written back over the
   // start of the slot (only this lane reads or writes its slots).  First round
   // in line (every lane runs the same code; lanes without a halo edge discard
@@ -940,8 +950,6 @@ __device__ __forceinline__ void facets_v2(const SFParams& p, const double* row, 
       for (int l = 0; l < NE; ++l) rho[ed][l] = fma(sj, FL[q * NE + l], rho[ed][l]);
     }
   }
-#pragma unroll
-  for (int m = 0; m < NBS; ++m) r[m] = 0.0;
   edge_test<K>(rho[0], rho[1], rho[2], r);
 }
 
@@ -1050,15 +1058,7 @@ conv2d_sf_kernel(SFParams p) {
       for (int m = 0; m < NBS; ++m) r[m] = 0.0;   // (not live across the traces)
     }
     if (F::RING) sf_rows_ring<K>(wc, gtile, s_prep, active ? le : 0, lane, N - F::FACET_ROWS, r, s_BT);
-    else {
-#ifdef HDGC_ROW_SPLIT
-      constexpr int NV = N - F::FACET_ROWS, H = HDGC_ROW_SPLIT;
-      sf_rows<K, 0, H>(wc, row, r, s_BT);
-      sf_rows<K, H, NV>(wc, row, r, s_BT);
-#else
-      sf_rows<K, 0, N - F::FACET_ROWS>(wc, row, r, s_BT);
-#endif
-    }
+    else sf_rows<K, 0, N - F::FACET_ROWS>(wc, row, r, s_BT);
     asm volatile("bar.sync 1, 64;\n" ::: "memory");   // (A) facet partial r ready, in-tile w reads done
     double racc = 0.0;   // STAGE: this lane's residual sum of squares
     if (active) {
@@ -1110,7 +1110,7 @@ conv2d_sf_kernel(SFParams p) {
     if (stopped) return;
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
     if constexpr (F::FV2) {
-      facets_v2<K>(p, row, wc, codes, sm + F::SM_TR, s_halo, T0, nel, lane, c, active, r);
+      facets_v2<K>(p, row, wc, codes, sm + F::SM_TR, s_halo, T0, nel, lane, c, active, r, s_BT);
     } else {
     double* halo = part;
     int halo_edge = -1;
@@ -1215,7 +1215,7 @@ conv2d_sf_kernel(SFParams p) {
     }
     }   // !FV2
     // balance: the facet warp also takes the last FACET_ROWS volume rows
-    if (F::FACET_ROWS > 0) sf_rows<K, N - F::FACET_ROWS, N>(wc, row, r, s_BT);
+    if (!F::FV2 && F::FACET_ROWS > 0) sf_rows<K, N - F::FACET_ROWS, N>(wc, row, r, s_BT);
     __syncwarp();          // halo reads of all lanes done before the partials overwrite it
 #pragma unroll
     for (int m = 0; m < NBS; ++m) part[m] = r[m];

@@ -200,3 +200,25 @@ def test_device_rules():
     for k in range(1, 9):
         assert B.volume_rule(k).weights.size == nqv[k - 1]
         assert B.facet_rule(k).weights.size == nf[k - 1]
+
+
+@pytest.mark.parametrize("k", range(1, 9))
+def test_dubiner_edge_trace_structure(k):
+    """The structure csrc/conv2d_sf.cuh's facets_v2 builds on (and sf_setup
+    re-checks on the uploaded tables): with R_e[l][m] = int_0^1 D_m(x_e(t)) L_l(t) dt,
+    R_0 is zero unless l == i, R_1 is zero for l > i + j, and
+    R_2[l][m] = (-1)^(i+l) R_1[l][m]   (m = (i, j) in dubiner_index order)."""
+    qf = B.facet_rule(k)
+    L = B.legendre_values(k, qf.points)                      # (nf, k+1)
+    R = [np.einsum("q,qm,ql->lm", qf.weights, B.dubiner_values(k, B.ref_edge_points(e, qf.points)), L)
+         for e in range(3)]
+    for m, (i, j) in enumerate(B.dubiner_index(k)):
+        for l in range(k + 1):
+            if l != i:
+                assert abs(R[0][l, m]) < 1e-13
+            if l > i + j:
+                assert abs(R[1][l, m]) < 1e-13
+            assert abs(R[2][l, m] - (-1) ** (i + l) * R[1][l, m]) < 1e-13
+    # the traces are exact: the expansion reproduces the point values
+    for e in range(3):
+        assert np.allclose(L @ R[e], B.dubiner_values(k, B.ref_edge_points(e, qf.points)), atol=1e-12)

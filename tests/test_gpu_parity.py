@@ -286,3 +286,26 @@ def test_zero_substeps_is_identity():
     w = F.transfer_I_host(m, k, u)
     op = ConvectionOperator(m, k)
     assert torch.equal(op.substeps(dev(u), dev(w), 1e-3, 0), dev(w))
+
+
+@pytest.mark.parametrize("k", [3, 4, 6, 7])
+def test_shuffled_element_order_halo_paths(k):
+    """Random element numbering on a jittered mesh: almost every neighbour of a
+    16-element tile lies outside it, so lanes have two or three halo edges (the
+    out-of-line halo rounds of facets_v2) and tiles ask for more than 32 halo
+    rows (the global-memory overflow path).  Apply + 6 substeps vs the C port."""
+    base = M.generate_jittered(12, 0.2, seed=3)
+    perm = np.random.default_rng(11).permutation(base.n_elements)
+    m = M.build_mesh(base.vertices, base.triangles[perm])
+    sf = F.StreamFunction(4, 7, (1.0, 0.3))
+    u = F.interpolate_curl(m, k, sf)
+    w = F.transfer_I_host(m, k, u)
+    inflow = F.inflow_values(m, k, sf)
+    op = ConvectionOperator(m, k)
+    port = P.PortOperator(m, k, threads=2)
+    assert rel(op.apply(dev(u), dev(w), dev(inflow)), port.apply(u, w, inflow)) < APPLY_TOL
+    wr = np.random.default_rng(5).standard_normal(w.shape)
+    assert rel(op.apply(dev(u), dev(wr), dev(inflow)), port.apply(u, wr, inflow)) < APPLY_TOL
+    dt = F.cfl_dt(m.h_min(), k, F.max_speed_host(m, k, u))
+    wd = op.substeps(dev(u), dev(w), dt, 6, dev(inflow))
+    assert rel(wd, port.substeps(u, w, dt, 6, inflow)) < SUBSTEP_TOL
