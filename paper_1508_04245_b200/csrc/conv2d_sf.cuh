@@ -67,9 +67,10 @@ struct SF {
   static constexpr int FACET_ROWS = HDGC_FACET_ROWS;
 #else
   // volume rows taken by the facet warp to balance the two warps (measured per
-  // k at 131k triangles: k=3 0/1 rows 38.1/37.0 us, k=4 2/3 rows 54.3/59.4 us,
-  // k=6 2/3/4 rows 165/176/189 us)
-  static constexpr int FACET_ROWS = K == 3 ? 1 : (K == 4 || K == 6) ? 2 : (K == 5 ? 1 : 0);
+  // k at 131k triangles with the mirror-pair rows and the one-round halo traces:
+  // k=3 0/1/2 rows 33.4/33.6/39.6 us, k=4 0/1/2 rows 46.0/46.8/54.6, k=6 1/2/3 rows
+  // 159/142/137.6)
+  static constexpr int FACET_ROWS = K == 3 ? 1 : K == 4 ? 1 : K == 6 ? 3 : (K == 5 ? 1 : 0);
 #endif
   static constexpr int PREP_TILE = PREP * 16;      // doubles per tile (EPB = 16)
 #ifdef HDGC_SF_RING
@@ -92,6 +93,21 @@ struct SF {
   // volume rows read w_c from the smem tile in every row instead of a register
   // copy (k=4: 121 registers without spills, 54.3 vs 55.5 us)
   static constexpr bool WSMEM = K == 4;
+#endif
+#ifdef HDGC_SYM
+  static constexpr bool SYM = HDGC_SYM;
+#else
+  // mirror-pair evaluation of the xi direction (sf_row) and of the facet points:
+  // k=3 34.7 vs 37.4 us, k=4 49.9 vs 55.0, k=6 146 vs 160 at 131k triangles; k=5
+  // (work-list facet stage, 186 registers) 119.8 vs 105.7: off there
+  static constexpr bool SYM = !RING && K != 5;
+#endif
+#ifdef HDGC_OWNF
+  static constexpr bool OWNF = HDGC_OWNF;
+#else
+  // facets_v2: own edge traces computed by the facet warp (no cross-warp barrier)
+  // instead of the volume warp
+  static constexpr bool OWNF = false;
 #endif
   static constexpr int RING_SLOT = 3 * N * 16;     // alpha | beta | gamma of one row, [3][N][16]
   // smem (doubles): mbarrier | prep tile [PREP][EPB] or ring [2][3][N][EPB] |
@@ -537,6 +553,52 @@ __device__ __forceinline__ void sf_row(const WS& wv, const double* al, const dou
   double Kc[NE];
 #pragma unroll
   for (int i = 0; i <= K; ++i) Kc[i] = 0.0;
+  if constexpr (F::SYM) {
+    // The xi points are Gauss-Legendre on [0, 1], symmetric about 1/2, and
+    // A_i(a) = P_i(2 xi_a - 1): A_i(N-1-a) = (-1)^i A_i(a), A'_i(N-1-a) =
+    // (-1)^(i+1) A'_i(a) (checked on the uploaded tables by sf_setup).  Values at
+    // a mirror pair from the even-i / odd-i partial sums, and the test through
+    // g(a) +- g(a'): 34 instead of 46 FP64 instructions per pair at k = 4.
+#pragma unroll
+    for (int a = 0; a < N / 2; ++a) {
+      const int a2 = N - 1 - a;
+      double ve = 0.0, vo = 0.0, ye = 0.0, yo = 0.0, xs = 0.0, xa = 0.0;
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        const double Ai = C[F::C_A + a * NE + i], Adi = C[F::C_AD + a * NE + i];
+        if (i & 1) {
+          vo = fma(Ai, Hw[i], vo);
+          yo = fma(Ai, Hwd[i], yo);
+          xs = fma(Adi, Hw[i], xs);
+        } else {
+          ve = fma(Ai, Hw[i], ve);
+          ye = fma(Ai, Hwd[i], ye);
+          xa = fma(Adi, Hw[i], xa);
+        }
+      }
+      const double g1 = fma(al[a * EPB], xs + xa, fma(be[a * EPB], ye + yo, ga[a * EPB] * (ve + vo)));
+      const double g2 = fma(al[a2 * EPB], xs - xa, fma(be[a2 * EPB], ye - yo, ga[a2 * EPB] * (ve - vo)));
+      const double gp = g1 + g2, gm = g1 - g2;
+#pragma unroll
+      for (int i = 0; i <= K; ++i) Kc[i] = fma((i & 1) ? gm : gp, C[F::C_A + a * NE + i], Kc[i]);
+    }
+    if constexpr (N & 1) {
+      // centre point xi = 1/2: odd-i values and even-i derivatives vanish
+      constexpr int a = N / 2;
+      double ve = 0.0, ye = 0.0, xs = 0.0;
+#pragma unroll
+      for (int i = 0; i <= K; ++i) {
+        if (i & 1) xs = fma(C[F::C_AD + a * NE + i], Hw[i], xs);
+        else {
+          ve = fma(C[F::C_A + a * NE + i], Hw[i], ve);
+          ye = fma(C[F::C_A + a * NE + i], Hwd[i], ye);
+        }
+      }
+      const double g = fma(al[a * EPB], xs, fma(be[a * EPB], ye, ga[a * EPB] * ve));
+#pragma unroll
+      for (int i = 0; i <= K; i += 2) Kc[i] = fma(g, C[F::C_A + a * NE + i], Kc[i]);
+    }
+  } else {
 #ifdef HDGC_A_UNROLL_SF
   constexpr int AU = F::RING ? HDGC_A_UNROLL : HDGC_A_UNROLL_SF;
 #else
@@ -555,6 +617,7 @@ __device__ __forceinline__ void sf_row(const WS& wv, const double* al, const dou
     const double g = fma(al[a * EPB], wxi, fma(be[a * EPB], wyy, ga[a * EPB] * wv0));
 #pragma unroll
     for (int i = 0; i <= K; ++i) Kc[i] = fma(g, C[F::C_A + a * NE + i], Kc[i]);
+  }
   }
 #pragma unroll
   for (int i = 0; i <= K; ++i) {
@@ -779,20 +842,6 @@ __device__ __forceinline__ void edge_test(const double (&rho0)[SF<K>::NE], const
   }
 }
 
-// One halo slot out of line (second and third halo edge of a lane): the
-// neighbour's trace on its edge e2 over the start of the slot.
-template <int K>
-__device__ __noinline__ void halo_trace_slot(double* slot, int e2) {
-  constexpr int NE = SF<K>::NE, NBS = SF<K>::NBS;
-  double nw[NBS];
-#pragma unroll
-  for (int m = 0; m < NBS; ++m) nw[m] = slot[m];
-  double a0[NE], a1[NE], a2[NE];
-  edge_traces<K>(nw, a0, a1, a2);
-#pragma unroll
-  for (int l = 0; l < NE; ++l) slot[l] = e2 == 1 ? a1[l] : (e2 == 2 ? a2[l] : a0[l]);
-}
-
 // More than 32 halo rows in one tile (not on the BASELINE meshes): the
 // neighbour's coefficients straight from global memory, rolled loops, out of line.
 template <int K>
@@ -843,23 +892,45 @@ __device__ __forceinline__ void facets_v2(const SFParams& p, const double* row, 
       }
     }
   }
-  // halo slots: lane-ordered claims per edge; slots >= 32 (rare) read global memory directly
+  // halo slots: lane-ordered claims per edge; slots >= 32 (rare) read global memory directly.
+  // The claiming lane starts the copy of the neighbour's coefficients into the slot;
+  // the neighbour's local edge id of slot s goes to bit s of two warp-wide masks.
   int hslot[3];
+  int nslots = 0;
+  unsigned e2lo = 0, e2hi = 0;
   {
-    int off = 0;
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int ed = 0; ed < 3; ++ed) {
       const bool need = (hmask >> ed) & 1u;
       const unsigned bal = __ballot_sync(0xffffffffu, need);
-      hslot[ed] = need ? off + __popc(bal & lt) : -1;
-      off += __popc(bal);
+      hslot[ed] = need ? nslots + __popc(bal & lt) : -1;
+      nslots += __popc(bal);
       if (need && hslot[ed] < 32) {
+        HDGC_ASSERT((codes[ed] >> 2) < p.nt && (codes[ed] & 3) < 3);
         const double* g = p.w + (size_t)(codes[ed] >> 2) * NB + c * NBS;
         double* dst = s_halo + hslot[ed] * HSTR;
 #pragma unroll
         for (int m = 0; m < NBS; ++m) cp_async8(dst + m, g + m);
+        e2lo |= (unsigned)(codes[ed] & 1) << hslot[ed];
+        e2hi |= (unsigned)((codes[ed] >> 1) & 1) << hslot[ed];
       }
+    }
+  }
+  if constexpr (F::OWNF) {
+    // own traces on the three edges -> s_tr row of this lane (own side of the
+    // jumps, and the in-tile neighbours), while the halo rows are in flight
+    double wv[NBS];
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) wv[m] = wc[m];
+    double t0[NE], t1[NE], t2[NE];
+    edge_traces<K>(wv, t0, t1, t2);
+    double* mine = s_tr + lane * HSTR;
+#pragma unroll
+    for (int l = 0; l < NE; ++l) {
+      mine[l] = t0[l];
+      mine[NE + l] = t1[l];
+      mine[2 * NE + l] = t2[l];
     }
   }
   // balance: the facet warp takes the last FACET_ROWS volume rows, while its halo
@@ -867,50 +938,31 @@ __device__ __forceinline__ void facets_v2(const SFParams& p, const double* row, 
 #pragma unroll
   for (int m = 0; m < NBS; ++m) r[m] = 0.0;
   if (F::FACET_ROWS > 0) sf_rows<K, N - F::FACET_ROWS, N>(wc, row, r, sBT);
-  // halo traces: the neighbour's trace on its edge e2, written back over the
-  // start of the slot (only this lane reads or writes its slots).  First round
-  // in line (every lane runs the same code; lanes without a halo edge discard
-  // the result), further rounds (a lane with two or three out-of-tile inflow
-  // edges: the ends of a tile) out of line.
-  unsigned pend = 0;
-#pragma unroll
-  for (int ed = 0; ed < 3; ++ed)
-    if (hslot[ed] >= 0 && hslot[ed] < 32) pend |= 1u << ed;
-  if (hmask) cp_async_wait_all();
-  if (__any_sync(0xffffffffu, pend != 0)) {
-    const double* src = wc;
-    double* dst = nullptr;
-    int e2 = 0;
-    if (pend) {
-      const int ed = __ffs(pend) - 1;
-      pend &= pend - 1;
-      const int slot = ed == 0 ? hslot[0] : (ed == 1 ? hslot[1] : hslot[2]);
-      const int code = ed == 0 ? codes[0] : (ed == 1 ? codes[1] : codes[2]);
-      HDGC_ASSERT((code >> 2) < p.nt && (code & 3) < 3);
-      dst = s_halo + slot * HSTR;
-      src = dst;
-      e2 = code & 3;
-    }
+  // halo traces: lane s evaluates the trace of slot s on the neighbour's edge and
+  // writes it back over the start of the slot -- one round whatever the number of
+  // out-of-tile inflow edges per lane (the ends of a tile have two or three).
+  // Every lane runs the same code; lanes without a slot discard the result.
+  if (nslots > 0) {   // warp-uniform
+    e2lo = __reduce_or_sync(0xffffffffu, e2lo);
+    e2hi = __reduce_or_sync(0xffffffffu, e2hi);
+    cp_async_wait_all();
+    __syncwarp();     // the slots were filled by other lanes' copies
+    const bool mine = lane < nslots;
+    double* dst = s_halo + lane * HSTR;
+    const double* src = mine ? dst : wc;
     double nw[NBS];
 #pragma unroll
     for (int m = 0; m < NBS; ++m) nw[m] = src[m];
+    const int e2 = (int)(((e2lo >> lane) & 1u) | (((e2hi >> lane) & 1u) << 1));
     double a0[NE], a1[NE], a2[NE];
     edge_traces<K>(nw, a0, a1, a2);
-    if (dst != nullptr) {
+    if (mine) {
 #pragma unroll
       for (int l = 0; l < NE; ++l) dst[l] = e2 == 1 ? a1[l] : (e2 == 2 ? a2[l] : a0[l]);
     }
-    while (__any_sync(0xffffffffu, pend != 0)) {
-      if (pend) {
-        const int ed = __ffs(pend) - 1;
-        pend &= pend - 1;
-        const int slot = ed == 0 ? hslot[0] : (ed == 1 ? hslot[1] : hslot[2]);
-        const int code = ed == 0 ? codes[0] : (ed == 1 ? codes[1] : codes[2]);
-        halo_trace_slot<K>(s_halo + slot * HSTR, code & 3);
-      }
-    }
   }
-  asm volatile("bar.sync 2, 64;\n" ::: "memory");   // (T) own traces of the tile published by the volume warp
+  if constexpr (F::OWNF) __syncwarp();   // own traces of the tile published by this warp
+  else asm volatile("bar.sync 2, 64;\n" ::: "memory");   // (T) own traces of the tile published by the volume warp
   double rho[3][NE];
 #pragma unroll
   for (int ed = 0; ed < 3; ++ed) {
@@ -938,6 +990,43 @@ __device__ __forceinline__ void facets_v2(const SFParams& p, const double* row, 
       rho[ed][l] = 0.0;
     }
     if (hslot[ed] >= 32) halo_overflow<K>(p.w + (size_t)(code >> 2) * NB + c * NBS, code & 3, own, dl);
+    if constexpr (F::SYM) {
+      // facet points are Gauss-Legendre on [0, 1]: L_l(t_{NF-1-q}) = (-1)^l L_l(t_q), so the
+      // jump at a mirror pair comes from the even-l / odd-l partial sums and the
+      // fold-back goes through sj(q) +- sj(q')
+#pragma unroll
+      for (int q = 0; q < NF / 2; ++q) {
+        const int q2 = NF - 1 - q;
+        const double s1 = on ? row[(F::P_S + ed * NF + q) * EPB] : 0.0;
+        const double s2 = on ? row[(F::P_S + ed * NF + q2) * EPB] : 0.0;
+        double Je = 0.0, Jo = 0.0;
+#pragma unroll
+        for (int l = 0; l < NE; ++l) {
+          if (l & 1) Jo = fma(dl[l], FL[q * NE + l], Jo);
+          else Je = fma(dl[l], FL[q * NE + l], Je);
+        }
+        double J1 = Je + Jo, J2 = Je - Jo;
+        if (infl != nullptr) {
+          if (s1 != 0.0) J1 += __ldg(infl + 2 * q);
+          if (s2 != 0.0) J2 += __ldg(infl + 2 * q2);
+        }
+        const double a1 = s1 * J1, a2 = s2 * J2;
+        const double sp = a1 + a2, sm = a1 - a2;
+#pragma unroll
+        for (int l = 0; l < NE; ++l) rho[ed][l] = fma((l & 1) ? sm : sp, FL[q * NE + l], rho[ed][l]);
+      }
+      if constexpr (NF & 1) {
+        constexpr int q = NF / 2;   // t = 1/2: odd-l values vanish
+        const double sq = on ? row[(F::P_S + ed * NF + q) * EPB] : 0.0;
+        double J = 0.0;
+#pragma unroll
+        for (int l = 0; l < NE; l += 2) J = fma(dl[l], FL[q * NE + l], J);
+        if (infl != nullptr && sq != 0.0) J += __ldg(infl + 2 * q);
+        const double sj = sq * J;
+#pragma unroll
+        for (int l = 0; l < NE; l += 2) rho[ed][l] = fma(sj, FL[q * NE + l], rho[ed][l]);
+      }
+    } else {
 #pragma unroll
     for (int q = 0; q < NF; ++q) {
       const double sq = on ? row[(F::P_S + ed * NF + q) * EPB] : 0.0;
@@ -948,6 +1037,7 @@ __device__ __forceinline__ void facets_v2(const SFParams& p, const double* row, 
       const double sj = sq * J;
 #pragma unroll
       for (int l = 0; l < NE; ++l) rho[ed][l] = fma(sj, FL[q * NE + l], rho[ed][l]);
+    }
     }
   }
   edge_test<K>(rho[0], rho[1], rho[2], r);
@@ -1038,7 +1128,7 @@ conv2d_sf_kernel(SFParams p) {
     mbar_wait(bar, 0);
     if (stopped) return;   // converged Richardson iteration: queued after the stop, writes nothing
     const double* wc = s_w + (active ? le : 0) * NB + c * NBS;
-    if constexpr (F::FV2) {
+    if constexpr (F::FV2 && !F::OWNF) {
       // own traces on the three edges -> s_tr row of this lane (read by the facet
       // warp: own side of the jumps, and the in-tile neighbours)
       double wv[NBS];
@@ -1054,6 +1144,8 @@ conv2d_sf_kernel(SFParams p) {
         mine[2 * NE + l] = t2[l];
       }
       asm volatile("bar.arrive 2, 64;\n" ::: "memory");   // (T)
+    }
+    if constexpr (F::FV2) {
 #pragma unroll
       for (int m = 0; m < NBS; ++m) r[m] = 0.0;   // (not live across the traces)
     }

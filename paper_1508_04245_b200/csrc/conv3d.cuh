@@ -19,6 +19,9 @@
 
 namespace hdgc {
 
+#ifndef HDGC_3D_SYM
+#define HDGC_3D_SYM 1   // mirror-pair evaluation of the a direction in the volume term
+#endif
 template <int K>
 struct Dims3 {
   static constexpr int NBS = (K + 1) * (K + 2) * (K + 3) / 6;
@@ -561,6 +564,54 @@ conv3d_kernel(Conv3Params p) {
           }
           H[i] = h; Hb[i] = hb; Hc[i] = hc; K1[i] = 0.0;
         }
+#if HDGC_3D_SYM
+        // The a points are Gauss-Legendre on [0, 1] and A_i(a) = P_i(2a - 1):
+        // A_i(N-1-ia) = (-1)^i A_i(ia), A'_i(N-1-ia) = (-1)^(i+1) A'_i(ia) (checked
+        // on the uploaded tables in create3d): values at a mirror pair from the
+        // even-i / odd-i partial sums, the test through g(ia) +- g(N-1-ia).
+#pragma unroll
+        for (int ia = 0; ia < N / 2; ++ia) {
+          const int i2 = N - 1 - ia;
+          double ve = 0.0, vo = 0.0, be = 0.0, bo = 0.0, ce = 0.0, co = 0.0, as = 0.0, aa = 0.0;
+#pragma unroll
+          for (int i = 0; i <= K; ++i) {
+            const double Ai = Cs[S::C_A + ia * NE + i], Adi = Cs[S::C_AD + ia * NE + i];
+            if (i & 1) {
+              vo = fma(Ai, H[i], vo);
+              bo = fma(Ai, Hb[i], bo);
+              co = fma(Ai, Hc[i], co);
+              as = fma(Adi, H[i], as);
+            } else {
+              ve = fma(Ai, H[i], ve);
+              be = fma(Ai, Hb[i], be);
+              ce = fma(Ai, Hc[i], ce);
+              aa = fma(Adi, H[i], aa);
+            }
+          }
+          const double g1 = fma(pal[ia], as + aa, fma(pbe[ia], be + bo, fma(pga[ia], ce + co, pde[ia] * (ve + vo))));
+          const double g2 = fma(pal[i2], as - aa, fma(pbe[i2], be - bo, fma(pga[i2], ce - co, pde[i2] * (ve - vo))));
+          const double gp = g1 + g2, gm = g1 - g2;
+#pragma unroll
+          for (int i = 0; i <= K; ++i) K1[i] = fma((i & 1) ? gm : gp, Cs[S::C_A + ia * NE + i], K1[i]);
+        }
+        if constexpr (N & 1) {
+          constexpr int ia = N / 2;   // a = 1/2: odd-i values and even-i derivatives vanish
+          double v = 0.0, va = 0.0, vb = 0.0, vc = 0.0;
+#pragma unroll
+          for (int i = 0; i <= K; ++i) {
+            if (i & 1) va = fma(Cs[S::C_AD + ia * NE + i], H[i], va);
+            else {
+              const double Ai = Cs[S::C_A + ia * NE + i];
+              v = fma(Ai, H[i], v);
+              vb = fma(Ai, Hb[i], vb);
+              vc = fma(Ai, Hc[i], vc);
+            }
+          }
+          const double g = fma(pal[ia], va, fma(pbe[ia], vb, fma(pga[ia], vc, pde[ia] * v)));
+#pragma unroll
+          for (int i = 0; i <= K; i += 2) K1[i] = fma(g, Cs[S::C_A + ia * NE + i], K1[i]);
+        }
+#else
 #pragma unroll
         for (int ia = 0; ia < N; ++ia) {
           double v = 0.0, va = 0.0, vb = 0.0, vc = 0.0;
@@ -576,6 +627,7 @@ conv3d_kernel(Conv3Params p) {
 #pragma unroll
           for (int i = 0; i <= K; ++i) K1[i] = fma(g, Cs[S::C_A + ia * NE + i], K1[i]);
         }
+#endif
 #pragma unroll
         for (int i = 0; i <= K; ++i)
 #pragma unroll

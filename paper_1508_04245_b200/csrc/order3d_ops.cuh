@@ -28,6 +28,19 @@ int launch3_setup(hdgc_ctx* c, const hdgc_tables_desc* t) {
   memcpy(&h[S::C_PF], t->col_pf, sizeof(double) * S::NQ * 5);
   // face modes at the face points: D2 = fac_L / 2 (fac_L is the normal-trace basis 2 D2)
   for (int i = 0; i < S::NF * S::NFD; ++i) h[S::C_D2 + i] = 0.5 * t->fac_L[i];
+#if HDGC_3D_SYM
+  {
+    // mirror symmetry of the a rule, used by the volume term of conv3d_kernel
+    double bad = 0.0;
+    for (int a = 0; a < S::N; ++a)
+      for (int i = 0; i <= K; ++i) {
+        const double sg = (i & 1) ? -1.0 : 1.0;
+        bad = fmax(bad, fabs(t->col_A[(S::N - 1 - a) * S::NE + i] - sg * t->col_A[a * S::NE + i]));
+        bad = fmax(bad, fabs(t->col_Ad[(S::N - 1 - a) * S::NE + i] + sg * t->col_Ad[a * S::NE + i]));
+      }
+    if (bad > 1e-12) return hdgc_set_err(HDGC_EINVAL, "3D collapsed tables are not mirror-symmetric in a (defect %.3e)", bad);
+  }
+#endif
   CUDA_TRY(cudaMemcpyToSymbol(c_sf3d, h.data(), sizeof(double) * S::C_TOTAL));
   // face trace maps R_f[n][m] = 2 sum_q w_q D_m(x_f(q)) D2_n(q)  (exact: degree 2k <= 3k+1)
   std::vector<double> R((size_t)4 * S::NFD * S::NBS, 0.0);

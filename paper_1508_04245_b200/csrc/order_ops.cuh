@@ -298,6 +298,24 @@ int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& 
         h[F::C_PB + b * F::N + a] = wp * t->col_xi[a] * t->col_inv1my[b];
         h[F::C_PW + b * F::N + a] = wp;
       }
+    if (F::SYM) {
+      // mirror symmetry of the xi rule and of the facet rule, used by sf_row / facets_v2:
+      // A_i(N-1-a) = (-1)^i A_i(a), A'_i(N-1-a) = (-1)^(i+1) A'_i(a), L_l(t_{NF-1-q}) = (-1)^l L_l(t_q)
+      double bad = 0.0;
+      for (int a = 0; a < F::N; ++a)
+        for (int i = 0; i <= K; ++i) {
+          const double sg = (i & 1) ? -1.0 : 1.0;
+          bad = fmax(bad, fabs(t->col_A[(F::N - 1 - a) * F::NE + i] - sg * t->col_A[a * F::NE + i]));
+          bad = fmax(bad, fabs(t->col_Ad[(F::N - 1 - a) * F::NE + i] + sg * t->col_Ad[a * F::NE + i]));
+        }
+      for (int q = 0; q < F::NF; ++q)
+        for (int l = 0; l < F::NE; ++l) {
+          const double sg = (l & 1) ? -1.0 : 1.0;
+          bad = fmax(bad, fabs(packed[D::OFF_FL + (F::NF - 1 - q) * F::NE + l] - sg * packed[D::OFF_FL + q * F::NE + l]));
+        }
+      if (bad > 1e-12)
+        return hdgc_set_err(HDGC_EINVAL, "collapsed / facet tables are not mirror-symmetric (defect %.3e)", bad);
+    }
     CUDA_TRY(cudaMemcpyToSymbol(c_sf, h.data(), sizeof(double) * F::C_TOTAL));
     CUDA_TRY(cudaMemcpyToSymbol(c_fd, &packed[D::OFF_FD], sizeof(double) * 3 * F::NF * F::NBS));
     CUDA_TRY(cudaMemcpyToSymbol(c_fl, &packed[D::OFF_FL], sizeof(double) * F::NF * F::NE));

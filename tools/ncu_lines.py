@@ -22,7 +22,13 @@ def main(rep, obj, top=30):
     rows = list(csv.reader(io.StringIO(txt)))
     kname = rows[0][1]
     h = rows[1]
-    data = [r for r in rows[2:] if len(r) == len(h)]
+    data = []
+    for r in rows[2:]:          # first launch only (a report may hold several)
+        if len(r) != len(h) or r[0] == h[0]:
+            if data:
+                break
+            continue
+        data.append(r)
     iS = h.index("Warp Stall Sampling (All Samples)")
     stall_cols = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
     base = int(data[0][0], 16)
