@@ -86,9 +86,9 @@ __device__ __forceinline__ double warp_sum_fixed(double a) {
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
   return a;
 }
-__device__ __forceinline__ void rich_cta_partial(const StageParams& st, double acc) {
+__device__ __forceinline__ void rich_cta_partial(const StageParams& st, double acc, int slot) {
   acc = warp_sum_fixed(acc);
-  if ((threadIdx.x & 31) == 0) st.rpart[blockIdx.x] = acc;
+  if ((threadIdx.x & 31) == 0) st.rpart[slot] = acc;
 }
 
 __device__ __forceinline__ bool stage_stopped(const StageParams& st) {
@@ -181,6 +181,10 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
                "r"(bytes)
                : "memory");
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+// L2 prefetch of a contiguous global range (16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");

@@ -84,6 +84,7 @@ struct hdgc_ctx {
   int64_t bytes = 0;
   int variant = 0;              // 0: thread-per-element (k <= 2), 1: sum-factorised (k >= 3)
   bool pdl = false;             // next update kernel may launch with PDL (set by hdgc_substeps only)
+  unsigned sweep = 0;           // launch counter of the sum-factorised update kernel (alternating tile sweeps)
   bool prep_dep = false;        // ... and it follows a prep kernel (stages the prep after griddepcontrol.wait)
 };
 

@@ -511,8 +511,12 @@ struct SFParams {
   // tile is the previous kernel's output and w is not: stage w (and the
   // tables) before griddepcontrol.wait, the prep tile after it
   int prep_dep;
+  int rev;   // 1: sweep the tiles from the last to the first (alternates from launch to launch)
 };
 
+#ifndef HDGC_PF_AHEAD
+#define HDGC_PF_AHEAD 0
+#endif
 #ifndef HDGC_A_UNROLL
 #define HDGC_A_UNROLL 2   // ring mode (k >= 7): measured k=8 474 us vs 572 us fully unrolled
 #endif
@@ -1071,7 +1075,11 @@ conv2d_sf_kernel(SFParams p) {
 
   double* s_x = sm + F::SM_X;              // STAGE: x tile [EPB][NB]
   hdgc_debug_prologue(sm, F::smem_doubles(MODE));
-  const int T0 = blockIdx.x * EPB;
+  // consecutive launches of a batch sweep the tiles in alternating directions
+  // (SFParams::rev): the tiles the previous substep touched last -- prep rows and
+  // its output w -- are the first ones read, while they are still in L2
+  const int tile = p.rev ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
+  const int T0 = tile * EPB;
   const int nel = min(EPB, p.nt - T0);
   double2* s_BT = reinterpret_cast<double2*>(sm + F::SM_BT);
   if (threadIdx.x == 0) {
@@ -1091,16 +1099,24 @@ conv2d_sf_kernel(SFParams p) {
       bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
       if (!F::FV2) bulk_g2s(s_fD, p.ftab, bt, bar);
       pdl_wait();
-      if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
+      if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)tile * F::PREP_TILE, bp, bar);
     } else {
       // substep batch: the prep tile is frozen, w is the previous update kernel's output
-      if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)blockIdx.x * F::PREP_TILE, bp, bar);
+      if (!F::RING) bulk_g2s(s_prep, p.prep + (size_t)tile * F::PREP_TILE, bp, bar);
       if (!F::FV2) bulk_g2s(s_fD, p.ftab, bt, bar);
       pdl_wait();
       bulk_g2s(s_w, p.w + (size_t)T0 * NB, bw, bar);
     }
     if (MODE == MODE_STAGE && F::XTILE)
       bulk_g2s(s_x, p.st.x + (size_t)T0 * NB, bw, bar);   // x is not the previous kernel's output
+#if HDGC_PF_AHEAD
+    // L2 prefetch of the prep tile a CTA HDGC_PF_AHEAD positions later in the sweep will stage
+    if (!F::RING) {
+      const int ahead = p.rev ? tile - HDGC_PF_AHEAD : tile + HDGC_PF_AHEAD;
+      if (ahead >= 0 && ahead < (int)gridDim.x)
+        bulk_prefetch_l2(p.prep + (size_t)ahead * F::PREP_TILE, (uint32_t)(F::PREP_TILE * sizeof(double)));
+    }
+#endif
   }
 
   const int warp = threadIdx.x >> 5;
@@ -1110,7 +1126,7 @@ conv2d_sf_kernel(SFParams p) {
   const bool active = le < nel;
   const int T = T0 + (active ? le : 0);
   double* part = s_halo + lane * F::HSTR;
-  const double* gtile = p.prep + (size_t)blockIdx.x * F::PREP_TILE;
+  const double* gtile = p.prep + (size_t)tile * F::PREP_TILE;
   // the element's prep column (slot j at row[j * EPB]): smem tile, or (ring) the global tile
   const double* row = (F::RING ? gtile : s_prep) + (active ? le : 0);
   double r[NBS];
@@ -1189,7 +1205,7 @@ conv2d_sf_kernel(SFParams p) {
       bulk_s2g(p.out + (size_t)T0 * NB, s_w, (uint32_t)(nel * NB * sizeof(double)));
       bulk_wait_read();
     }
-    if (MODE == MODE_STAGE && p.st.rpart) rich_cta_partial(p.st, racc);
+    if (MODE == MODE_STAGE && p.st.rpart) rich_cta_partial(p.st, racc, tile);
   } else {
     // ===================== facet warp =====================
     int codes[3];

@@ -336,7 +336,7 @@ conv2d_sfm_kernel(SFParams p) {
       bulk_s2g(p.out + (size_t)T0 * NB, s_w, (uint32_t)(nel * NB * sizeof(double)));
       bulk_wait_read();
     }
-    if (MODE == MODE_STAGE && p.st.rpart) rich_cta_partial(p.st, racc);
+    if (MODE == MODE_STAGE && p.st.rpart) rich_cta_partial(p.st, racc, (int)blockIdx.x);
   } else {
     // ===================== facet warp =====================
     int codes[3];

@@ -171,6 +171,9 @@ bool modal_enabled() {
 
 template <int K>
 int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
+  // the prep writes its tiles first to last: the update kernel after it sweeps
+  // last to first and finds the newest prep tiles in L2 (SFParams::rev)
+  c->sweep = 1;
   if constexpr (K >= 3 && K <= 6) {
     if (c->modal) {
       const int smem = PrepMma<K>::SMEM * (int)sizeof(double);
@@ -236,6 +239,9 @@ int sf_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, double
     p.st = sp;
     p.nt = c->nt;
     p.prep_dep = c->prep_dep ? 1 : 0;
+    // HDGC_ZIGZAG=0: every launch sweeps forward (development A/B)
+    static const bool zigzag = [] { const char* e = getenv("HDGC_ZIGZAG"); return !(e && e[0] == '0'); }();
+    p.rev = zigzag ? (int)(c->sweep++ & 1u) : 0;
     if constexpr (K <= 6) {
       // three-warp kernel (conv2d_sfm.cuh): modal prep, or (HDGC_SFM3=1) the point prep
       static const bool sfm3 = [] { const char* e = getenv("HDGC_SFM3"); return e && e[0] == '1'; }();
