@@ -349,6 +349,17 @@ def main():
         measured_flop = ncu_fp64_flop(nc)
     except Exception:
         pass
+    # in-stream traffic: single-pass ncu capture of a substep batch without cache
+    # flushes (tools/dram_instream.py) -- what a launch moves when the L2 holds
+    # what the previous launch of the batch left (alternating sweeps)
+    traffic_in = None
+    in_src = _latest_profile("dram_instream_k4_r*.json")
+    try:
+        with open(in_src) as fh:
+            di = json.load(fh)
+        traffic_in = di["dram_read_bytes_median"] + di["dram_write_bytes_median"]
+    except Exception:
+        pass
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = cpu_baseline_sample(m, u, w, inflow, dt)
@@ -373,7 +384,12 @@ def main():
                      "hw_fp64_frac": (measured_flop / k_s / 1e12 / dfma_peak) if measured_flop else None,
                      "hw_fp64_peak_tflops": dfma_peak,
                      "hw_dram_frac": (traffic / k_s / 1e9 / hbm) if traffic else None,
-                     "traffic_over_algorithmic": (traffic / (NT * byts)) if traffic else None},
+                     "traffic_over_algorithmic": (traffic / (NT * byts)) if traffic else None,
+                     # the same with the in-stream (warm L2, alternating sweeps) DRAM bytes per launch
+                     "traffic_instream": traffic_in,
+                     "traffic_instream_source": os.path.relpath(in_src, ROOT) if in_src else None,
+                     "hw_dram_frac_instream": (traffic_in / k_s / 1e9 / hbm) if traffic_in else None,
+                     "traffic_instream_over_algorithmic": (traffic_in / (NT * byts)) if traffic_in else None},
         "cpu_baseline": cpu,
         "e2e": {"value": world * dofs_per_step / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": int(u.nbytes + w.nbytes + inflow.nbytes),

@@ -115,6 +115,7 @@ struct ElemParams {
   const int32_t* __restrict__ code;   // (NT, 3)
   const double* __restrict__ piola;   // (4, NT) SoA: J/detJ row-major (00, 01, 10, 11)
   const double* __restrict__ minv;    // (NT,) 2/detJ
+  const double* __restrict__ prep = nullptr;   // frozen-velocity rows (prep_thread2d_kernel) or nullptr
   double* __restrict__ out;           // (NT, NB)
   StageParams st;
   int nt;

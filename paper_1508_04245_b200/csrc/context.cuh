@@ -84,6 +84,9 @@ struct hdgc_ctx {
   int64_t bytes = 0;
   int variant = 0;              // 0: thread-per-element (k <= 2), 1: sum-factorised (k >= 3)
   bool pdl = false;             // next update kernel may launch with PDL (set by hdgc_substeps only)
+  double* d_tprep = nullptr;    // k <= 2: frozen-velocity rows of prep_thread2d_kernel (allocated on first use)
+  bool tprep_valid = false;     // d_tprep holds the rows of the u last passed to prep_any
+  bool tprep_on = false;        // the next thread-variant launch reads d_tprep (set by apply_any_)
   unsigned sweep = 0;           // launch counter of the sum-factorised update kernel (alternating tile sweeps)
   bool prep_dep = false;        // ... and it follows a prep kernel (stages the prep after griddepcontrol.wait)
 };
@@ -97,6 +100,7 @@ namespace hdgc {
 // per-order operations, explicitly instantiated in order_k<K>.cu
 template <int K> int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w,
                                  const double* inflow, double* out, const StageParams& sp, cudaStream_t st);
+template <int K> int launch_elem_prep(hdgc_ctx* c, const double* u, cudaStream_t st);
 template <int K> int launch_transfer(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st);
 template <int K> int launch_maxspeed(hdgc_ctx* c, const double* u, double* out, cudaStream_t st);
 template <int K> int sf_prep(hdgc_ctx* c, const double* u, cudaStream_t st);
@@ -128,5 +132,6 @@ template <int K> int launch3_setup(hdgc_ctx* c, const hdgc_tables_desc* t);
   extern template int sf_prep<K>(hdgc_ctx*, const double*, cudaStream_t);                          \
   extern template int sf_main<K>(hdgc_ctx*, int, const double*, const double*, double*, const StageParams&, \
                                  cudaStream_t);                                                    \
-  extern template int sf_setup<K>(hdgc_ctx*, const hdgc_tables_desc*, const std::vector<double>&);
+  extern template int sf_setup<K>(hdgc_ctx*, const hdgc_tables_desc*, const std::vector<double>&); \
+  extern template int launch_elem_prep<K>(hdgc_ctx*, const double*, cudaStream_t);
 }  // namespace hdgc

@@ -49,7 +49,91 @@ __host__ __device__ constexpr int thread_smem_bytes() {
   return (thread_fd_doubles<K>() + (HDGC_THR_TMA ? 2 * THREAD_BLOCK * Dims<K>::NB : 0)) * 8;
 }
 
-template <int K, int MODE>
+// Frozen-velocity prep of the thread variant (substep batches, hdgc_propagate,
+// Richardson: u is frozen over the batch): per element the
+// velocity at the NQV volume points, u_hat_0(q), u_hat_1(q), div u_hat(q), and
+// the inflow weights s_e(q) = w_q F_e(t_q) where F < 0 (else 0), evaluated with
+// the same FMA sequences as the update kernel uses without a prep (so both
+// paths give bitwise identical results); the update kernels then neither redo
+// the modal transform (NB^2 FMA) nor the velocity evaluation.
+// Quadrature-point data, not an assembled matrix.
+// Layout [cta][slot][THREAD_BLOCK]: coalesced for writer and readers.
+template <int K>
+struct ThreadPrep {
+  static constexpr int NQV = Dims<K>::NQV, NF = Dims<K>::NF;
+  static constexpr int S_FAC = 3 * NQV;
+  static constexpr int SLOTS = 3 * NQV + 3 * NF;
+};
+
+template <int K>
+__global__ void __launch_bounds__(THREAD_BLOCK)
+prep_thread2d_kernel(const double* __restrict__ u, int nt, double* __restrict__ prep) {
+  static_assert(K == HDGC_ORDER && K <= 2, "thread variant: k <= 2, tables per translation unit");
+  using D = Dims<K>;
+  using TP = ThreadPrep<K>;
+  constexpr int NB = D::NB, NBS = D::NBS, NBS1 = D::NBS1, NE = D::NE, NF = D::NF, NQV = D::NQV;
+  const double* coef = c_th + D::OFF_COEF;
+  const double* divm = c_th + D::OFF_DIVM;
+  const double* vD = c_th + D::OFF_VD;
+  const double* fw = c_th + D::OFF_FW;
+  const double* fL = c_th + D::OFF_FL;
+  const double* flen = c_th + D::OFF_FLEN;
+  const int T = blockIdx.x * blockDim.x + threadIdx.x;
+  if (T >= nt) return;
+  double* out = prep + (size_t)blockIdx.x * TP::SLOTS * THREAD_BLOCK + threadIdx.x;
+  double x[NB];
+  {
+    const double2* ug = reinterpret_cast<const double2*>(u + (size_t)T * NB);
+#pragma unroll
+    for (int j = 0; j < NB / 2; ++j) {
+      const double2 t = __ldg(ug + j);
+      x[2 * j] = t.x;
+      x[2 * j + 1] = t.y;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 3; ++e) {
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      double a = 0.0;
+#pragma unroll
+      for (int l = 0; l < NE; ++l) a = fma(x[e * NE + l], fL[q * NE + l], a);
+      const double Fq = a * flen[e];
+      out[(TP::S_FAC + e * NF + q) * THREAD_BLOCK] = Fq < 0.0 ? fw[q] * Fq : 0.0;
+    }
+  }
+  double uh[NB], dv[NBS1];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    double a = 0.0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) a = fma(coef[i * NB + j], x[j], a);
+    uh[i] = a;
+  }
+#pragma unroll
+  for (int i = 0; i < NBS1; ++i) {
+    double a = 0.0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) a = fma(divm[i * NB + j], x[j], a);
+    dv[i] = a;
+  }
+#pragma unroll
+  for (int q = 0; q < NQV; ++q) {
+    const double* Dq = vD + q * NBS;
+    double u0 = 0.0, u1 = 0.0, dvq = 0.0;
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) {
+      u0 = fma(uh[m], Dq[m], u0);
+      u1 = fma(uh[NBS + m], Dq[m], u1);
+      if (m < NBS1) dvq = fma(dv[m], Dq[m], dvq);
+    }
+    out[(3 * q + 0) * THREAD_BLOCK] = u0;
+    out[(3 * q + 1) * THREAD_BLOCK] = u1;
+    out[(3 * q + 2) * THREAD_BLOCK] = dvq;
+  }
+}
+
+template <int K, int MODE, bool PREP = false>
 #ifndef HDGC_THR_MINB2
 #define HDGC_THR_MINB2 8
 #endif
@@ -93,16 +177,27 @@ conv2d_thread_kernel(ElemParams p) {
   for (int i = threadIdx.x; i < 3 * NF * NBS; i += blockDim.x) s_fD[i] = p.tab[D::OFF_FD + i];
   if (HDGC_THR_TMA) {
     __syncthreads();   // mbarrier init visible
-    if (threadIdx.x == 0) {
+    if (!PREP && threadIdx.x == 0) {
       mbar_arrive_expect_tx(&tbar[0], (uint32_t)(nel * NB * sizeof(double)));
       bulk_g2s(s_u, p.u + (size_t)tb * NB, (uint32_t)(nel * NB * sizeof(double)), &tbar[0]);
     }
   }
 
+  // PREP: the frozen-velocity rows of this element (prep_thread2d_kernel), all loads
+  // in flight before griddepcontrol.wait
+  using TP = ThreadPrep<K>;
+  double pa[PREP ? 3 * NQV : 1], ps[PREP ? 3 * NF : 1];
+  if constexpr (PREP) {
+    const double* pr = p.prep + (size_t)blockIdx.x * TP::SLOTS * THREAD_BLOCK + threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < 3 * NQV; ++i) pa[i] = __ldg(pr + (size_t)i * THREAD_BLOCK);
+#pragma unroll
+    for (int i = 0; i < 3 * NF; ++i) ps[i] = __ldg(pr + (size_t)(TP::S_FAC + i) * THREAD_BLOCK);
+  }
   // modal velocity u_hat = coef u and its modal divergence dv = divm u (in P_{k-1})
   double uh[NB];
   double dv[NBS1];
-  {
+  if constexpr (!PREP) {
     double u[NB];
     if (HDGC_THR_TMA) {
       mbar_wait(&tbar[0], 0);
@@ -180,13 +275,20 @@ conv2d_thread_kernel(ElemParams p) {
       const double d = Dq[m], gx = Gq[2 * m], gy = Gq[2 * m + 1];
       w0 = fma(w[m], d, w0);
       w1 = fma(w[NBS + m], d, w1);
-      u0 = fma(uh[m], d, u0);
-      u1 = fma(uh[NBS + m], d, u1);
+      if constexpr (!PREP) {
+        u0 = fma(uh[m], d, u0);
+        u1 = fma(uh[NBS + m], d, u1);
+        if (m < NBS1) dvq = fma(dv[m], d, dvq);
+      }
       w0x = fma(w[m], gx, w0x);
       w0y = fma(w[m], gy, w0y);
       w1x = fma(w[NBS + m], gx, w1x);
       w1y = fma(w[NBS + m], gy, w1y);
-      if (m < NBS1) dvq = fma(dv[m], d, dvq);
+    }
+    if constexpr (PREP) {
+      u0 = pa[3 * q];
+      u1 = pa[3 * q + 1];
+      dvq = pa[3 * q + 2];
     }
     const double wt = vw[q];
     const double f0 = wt * fma(u0, w0x, fma(u1, w0y, w0 * dvq));
@@ -202,19 +304,27 @@ conv2d_thread_kernel(ElemParams p) {
   // ---- facets: upwind jump on inflow points only (element-owned, no atomics)
 #pragma unroll
   for (int e = 0; e < 3; ++e) {
-    double ue[NE];
-#pragma unroll
-    for (int l = 0; l < NE; ++l) ue[l] = HDGC_THR_TMA ? s_u[(T - tb) * NB + e * NE + l] : __ldg(p.u + (size_t)T * NB + e * NE + l);
-    const double len = flen[e];
-    double F[NF];
+    double F[NF];   // PREP: the inflow weights s_q (0 where F >= 0), else F itself
     bool inflow_edge = false;
+    if constexpr (PREP) {
 #pragma unroll
-    for (int q = 0; q < NF; ++q) {
-      double a = 0.0;
+      for (int q = 0; q < NF; ++q) {
+        F[q] = ps[e * NF + q];
+        inflow_edge |= F[q] != 0.0;
+      }
+    } else {
+      double ue[NE];
 #pragma unroll
-      for (int l = 0; l < NE; ++l) a = fma(ue[l], fL[q * NE + l], a);
-      F[q] = a * len;
-      inflow_edge |= F[q] < 0.0;
+      for (int l = 0; l < NE; ++l) ue[l] = HDGC_THR_TMA ? s_u[(T - tb) * NB + e * NE + l] : __ldg(p.u + (size_t)T * NB + e * NE + l);
+      const double len = flen[e];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) {
+        double a = 0.0;
+#pragma unroll
+        for (int l = 0; l < NE; ++l) a = fma(ue[l], fL[q * NE + l], a);
+        F[q] = a * len;
+        inflow_edge |= F[q] < 0.0;
+      }
     }
     if (!inflow_edge) continue;  // pure outflow edge: w_hat = own trace, jump = 0
     const int code = __ldg(p.code + (size_t)T * 3 + e);
@@ -242,7 +352,7 @@ conv2d_thread_kernel(ElemParams p) {
 #pragma unroll
     for (int q = 0; q < NF; ++q) {
       const double Fq = F[q];
-      if (!(Fq < 0.0)) continue;
+      if (PREP ? Fq == 0.0 : !(Fq < 0.0)) continue;
       const double* De = fD + (e * NF + q) * NBS;
       double o0 = 0.0, o1 = 0.0;
 #pragma unroll
@@ -263,7 +373,7 @@ conv2d_thread_kernel(ElemParams p) {
         x0 = __ldg(infl + 2 * q);
         x1 = __ldg(infl + 2 * q + 1);
       }
-      const double s = fw[q] * Fq;
+      const double s = PREP ? Fq : fw[q] * Fq;
       const double j0 = s * (x0 - o0), j1 = s * (x1 - o1);
 #pragma unroll
       for (int m = 0; m < NBS; ++m) {

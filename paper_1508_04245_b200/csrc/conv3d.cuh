@@ -414,6 +414,7 @@ struct Conv3Params {
   int nt;
   int ps;    // SoA stride of the face slots (prep3_stride)
   int prep_dep;   // 1: launched (PDL) right after the prep: stage its rows after griddepcontrol.wait
+  int rev;        // 1: sweep the element blocks last to first (alternates from launch to launch)
 };
 
 // one thread per (element, component); warp w of the CTA = component w of 32
@@ -425,7 +426,10 @@ conv3d_kernel(Conv3Params p) {
   constexpr int NB = D::NB, NBS = D::NBS, NQ = D::NQ, NF = D::NF;
   if (MODE == MODE_STAGE && stage_stopped(p.st)) return;   // converged Richardson iteration
   const int c = threadIdx.x / D::EPB;
-  const int T0 = blockIdx.x * D::EPB + (threadIdx.x % D::EPB);
+  // alternating sweeps (Conv3Params::rev, as in conv2d_sf_kernel): the rows the
+  // previous kernel touched last are read first, while they are still in L2
+  const int tile = p.rev ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
+  const int T0 = tile * D::EPB + (threadIdx.x % D::EPB);
   const bool active = T0 < p.nt;
   const int T = active ? T0 : p.nt - 1;
   const double* tab = p.tab;
@@ -448,7 +452,7 @@ conv3d_kernel(Conv3Params p) {
   // against the generic-proxy reads) and refills the buffer NRB rows ahead.
   // Nothing here depends on the previous kernel, so the first NRB rows go
   // before griddepcontrol.wait.
-  const double* vtile = p.prep + (size_t)(blockIdx.x) * D::NROW * D::RBUF;
+  const double* vtile = p.prep + (size_t)tile * D::NROW * D::RBUF;
   auto issue_first_rows = [&]() {
 #pragma unroll
     for (int r = 0; r < D::NRB && r < D::NROW; ++r) {
@@ -779,7 +783,7 @@ conv3d_kernel(Conv3Params p) {
       guard_finite(p.st.flag, chk);
     }
     __syncthreads();   // every warp is done with s_wo / s_wn
-    const int tb = blockIdx.x * D::EPB, nel = min(D::EPB, p.nt - tb), e = threadIdx.x % D::EPB;
+    const int tb = tile * D::EPB, nel = min(D::EPB, p.nt - tb), e = threadIdx.x % D::EPB;
     double* s_out = s_wo;   // [EPB][NB] row-major (fits in s_wo | s_wn)
     if (active) {
 #pragma unroll

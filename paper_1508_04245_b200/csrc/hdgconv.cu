@@ -423,6 +423,10 @@ static int elem(hdgc_ctx* c, int mode, const double* u, const double* w, const d
                 const StageParams& sp, cudaStream_t st) {
   HDGC_K_SWITCH(c->k, launch_elem<KK>(c, mode, u, w, inflow, out, sp, st));
 }
+// k <= 2: frozen-velocity rows for a batch of update kernels on the same u
+static int elem_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
+  HDGC_K_SWITCH(c->k, launch_elem_prep<KK>(c, u, st));
+}
 
 static int transfer3(hdgc_ctx* c, int dir, const double* in, double* out, cudaStream_t st);
 
@@ -503,7 +507,12 @@ static int apply_any_(hdgc_ctx* c, int mode, const double* u, const double* w, c
     if (rc) return rc;
     return after_prep(c, sfmain, mode, w, inflow, out, sp, st);
   }
-  return elem(c, mode, u, w, inflow, out, sp, st);
+  // thread variant (k <= 2): the update kernels read the frozen-velocity rows when
+  // the caller prepared them for this u (prep_any), else they evaluate u themselves
+  c->tprep_on = prep_done && c->tprep_valid && (mode == MODE_SUBSTEP || mode == MODE_STAGE);
+  const int rc = elem(c, mode, u, w, inflow, out, sp, st);
+  c->tprep_on = false;
+  return rc;
 }
 static int apply_any(hdgc_ctx* c, int mode, const double* u, const double* w, const double* inflow, double* out,
                      double dt, bool prep_done, cudaStream_t st) {
@@ -511,10 +520,17 @@ static int apply_any(hdgc_ctx* c, int mode, const double* u, const double* w, co
   sp.c = -dt;
   return apply_any(c, mode, u, w, inflow, out, sp, prep_done, st);
 }
-static int prep_any(hdgc_ctx* c, const double* u, cudaStream_t st) {
+// uses: how many update kernels will run on this frozen u (the thread variant's
+// prep costs about 0.6 of an update kernel and saves about a third of each)
+static int prep_any(hdgc_ctx* c, const double* u, cudaStream_t st, int uses = 1 << 20) {
   if (c->variant == 2) return prep3(c, u, st);
   if (c->variant == 1) return prep(c, u, st);
-  return HDGC_OK;
+  static const bool tprep = [] { const char* e = getenv("HDGC_TPREP"); return !(e && e[0] == '0'); }();
+  c->tprep_valid = false;
+  if (!tprep || uses < 3 || c->dim != 2) return HDGC_OK;
+  const int rc = elem_prep(c, u, st);
+  c->tprep_valid = rc == HDGC_OK;
+  return rc;
 }
 
 // ---------------------------------------------------------------------------
@@ -900,9 +916,9 @@ static int substeps_enqueue(hdgc_ctx* c, const double* u, double* w, const doubl
                             cudaStream_t st) {
   double* a = w;
   double* b = c->d_scratch;
-  if (nsteps > 0 && c->variant >= 1) {
+  if (nsteps > 0) {
     // u is frozen over the substep batch: one prep per batch
-    int rc = c->variant == 2 ? prep3(c, u, st) : prep(c, u, st);
+    int rc = prep_any(c, u, st, nsteps);
     if (rc) return rc;
   }
   for (int s = 0; s < nsteps; ++s) {
@@ -1025,7 +1041,7 @@ int hdgc_propagate(hdgc_ctx* c, const double* u_prev, const double* u_cur, doubl
   auto velocity = [&](double s, const double** uu) -> int {
     if (!u_prev) {
       *uu = u_cur;
-      if (!have) { have = true; after_update = false; return prep_any(c, u_cur, st); }
+      if (!have) { have = true; after_update = false; return prep_any(c, u_cur, st, nsteps * (scheme + 1)); }
       return HDGC_OK;
     }
     *uu = c->d_uext;
@@ -1036,7 +1052,7 @@ int hdgc_propagate(hdgc_ctx* c, const double* u_prev, const double* u_cur, doubl
     CUDA_TRY(cudaGetLastError());
     have = true;
     at = s;
-    return prep_any(c, c->d_uext, st);
+    return prep_any(c, c->d_uext, st, scheme + 1);   // one prep per pseudo-time level
   };
   double* bufs[3] = {w, c->d_scratch, c->d_scratch2};
   const int nbuf = scheme == 1 ? 3 : 2;   // Euler ping-pongs, Heun rotates v, v1, v'

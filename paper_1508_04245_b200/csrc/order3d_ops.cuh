@@ -70,6 +70,7 @@ int launch3_setup(hdgc_ctx* c, const hdgc_tables_desc* t) {
 
 template <int K>
 int launch3_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
+  c->sweep = 1;   // the update kernel after a prep sweeps last to first (newest prep rows in L2)
   Prep3Params p;
   p.tab = c->d_tab;
   p.u = u;
@@ -113,6 +114,8 @@ int launch3_main(hdgc_ctx* c, int mode, const double* w, const double* inflow, d
   p.nt = c->nt;
   p.ps = prep3_stride(c->nt);
   p.prep_dep = c->prep_dep ? 1 : 0;
+  static const bool zigzag = [] { const char* e = getenv("HDGC_ZIGZAG"); return !(e && e[0] == '0'); }();
+  p.rev = zigzag ? (int)(c->sweep++ & 1u) : 0;
   const unsigned blocks = grid3_for(c->nt, Dims3<K>::EPB);
   constexpr int smem = Dims3<K>::SMEM;
   auto launch = [&](auto kern) -> int {

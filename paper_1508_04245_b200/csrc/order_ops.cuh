@@ -113,6 +113,11 @@ int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w, const d
     CUDA_TRY(launch_maybe_pdl(kern, blocks, threads, smem, st, c->pdl, p));
     return HDGC_OK;
   };
+  if (c->tprep_on && c->d_tprep) {
+    p.prep = c->d_tprep;
+    if (mode == MODE_SUBSTEP) return launch(conv2d_thread_kernel<K, MODE_SUBSTEP, true>);
+    if (mode == MODE_STAGE) return launch(conv2d_thread_kernel<K, MODE_STAGE, true>);
+  }
   switch (mode) {
     case MODE_APPLY: return launch(conv2d_thread_kernel<K, MODE_APPLY>);
     case MODE_SUBSTEP: return launch(conv2d_thread_kernel<K, MODE_SUBSTEP>);
@@ -120,6 +125,25 @@ int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w, const d
     default: return launch(conv2d_thread_kernel<K, MODE_APPLY_IT>);
   }
  }
+}
+
+// frozen-velocity rows of the thread variant (k <= 2) into c->d_tprep
+template <int K>
+int launch_elem_prep(hdgc_ctx* c, const double* u, cudaStream_t st) {
+  if constexpr (K > 2) {
+    (void)c; (void)u; (void)st;
+    return hdgc_set_err(HDGC_EUNSUP, "thread-per-element variant is built for k <= 2 only");
+  } else {
+    const int blocks = (c->nt + THREAD_BLOCK - 1) / THREAD_BLOCK;
+    if (!c->d_tprep) {
+      const int rc = hdgc_dev_alloc(c, (void**)&c->d_tprep,
+                                    sizeof(double) * (size_t)blocks * ThreadPrep<K>::SLOTS * THREAD_BLOCK);
+      if (rc) return rc;
+    }
+    prep_thread2d_kernel<K><<<blocks, THREAD_BLOCK, 0, st>>>(u, c->nt, c->d_tprep);
+    CUDA_TRY(cudaGetLastError());
+    return HDGC_OK;
+  }
 }
 
 template <int K>
@@ -420,6 +444,7 @@ int sf_setup(hdgc_ctx* c, const hdgc_tables_desc* t, const std::vector<double>& 
   namespace hdgc {                                                                                \
   template int launch_elem<K>(hdgc_ctx*, int, const double*, const double*, const double*, double*, \
                               const StageParams&, cudaStream_t);                                              \
+  template int launch_elem_prep<K>(hdgc_ctx*, const double*, cudaStream_t);                      \
   template int launch_transfer<K>(hdgc_ctx*, int, const double*, double*, cudaStream_t);          \
   template int launch_maxspeed<K>(hdgc_ctx*, const double*, double*, cudaStream_t);               \
   template int sf_prep<K>(hdgc_ctx*, const double*, cudaStream_t);                                \
