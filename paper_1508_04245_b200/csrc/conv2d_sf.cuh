@@ -432,21 +432,30 @@ prep_tile2d_kernel(const double* __restrict__ tab, const double* __restrict__ af
   }
   for (int i = tid; i < (P::KS * 4 - NB) * 32; i += NTH) s_u[(NB + i / 32) * LD + (i & 31)] = 0.0;
   __syncthreads();
-  // stage 1: (MT x 4) output tiles of 8 x 8 over the warps
-  for (int t = warp; t < P::MT * 4; t += N) {
-    const int mt = t >> 2, n0 = (t & 3) * 8;
+  // stage 1: MT row tiles of 8 x 32 over the warps; the four 8 x 8 column tiles of a
+  // row tile share each A fragment and run as four independent DMMA chains (a
+  // single chain per 8 x 8 tile serialised KS dependent DMMAs per tile)
+  for (int mt = warp; mt < P::MT; mt += N) {
     const double* af = afrag + (size_t)mt * P::KS * 32 + lane;
-    double d0 = 0.0, d1 = 0.0;
+    double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-    for (int ks = 0; ks < P::KS; ++ks)
-      dmma_m8n8k4(d0, d1, __ldg(af + ks * 32), s_u[(ks * 4 + (lane & 3)) * LD + n0 + (lane >> 2)]);
-    *reinterpret_cast<double2*>(s_h + (mt * 8 + (lane >> 2)) * LD + n0 + 2 * (lane & 3)) = make_double2(d0, d1);
+    for (int ks = 0; ks < P::KS; ++ks) {
+      const double a = __ldg(af + ks * 32);
+      const double* bs = s_u + (ks * 4 + (lane & 3)) * LD + (lane >> 2);
+#pragma unroll
+      for (int nq = 0; nq < 4; ++nq) dmma_m8n8k4(d[nq][0], d[nq][1], a, bs[nq * 8]);
+    }
+#pragma unroll
+    for (int nq = 0; nq < 4; ++nq)
+      *reinterpret_cast<double2*>(s_h + (mt * 8 + (lane >> 2)) * LD + nq * 8 + 2 * (lane & 3)) =
+          make_double2(d[nq][0], d[nq][1]);
   }
   const bool active = lane < nel;
   double* out = prep + (size_t)(blockIdx.x * 2 + (lane >> 4)) * F::PREP_TILE + (lane & 15);
-  if (warp < 3 && active) {
-    // inflow weights of edge `warp`: F = |e| sum_l u[e(k+1)+l] L_l(t_q)
-    const int ed = warp;
+  if (warp >= N - 3 && active) {
+    // inflow weights of edge N-1-warp (the last warps: they have the fewest row
+    // tiles in stage 1): F = |e| sum_l u[e(k+1)+l] L_l(t_q)
+    const int ed = N - 1 - warp;
     const double len = __ldg(tab + D::OFF_FLEN + ed);
     const double* FL = fl_tab<K>();
 #pragma unroll

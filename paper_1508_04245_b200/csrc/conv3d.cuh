@@ -273,14 +273,22 @@ prep_tile3d_kernel(const double* __restrict__ tab, const double* __restrict__ af
   for (int i = tid; i < (P::KS * 4 - NB) * 32; i += NTH) s_u[(NB + i / 32) * LD + (i & 31)] = 0.0;
   if (tid < 32) s_mask[tid] = 0u;
   __syncthreads();
-  for (int t = warp; t < P::MT * 4; t += P::WARPS) {
-    const int mt = t >> 2, n0 = (t & 3) * 8;
+  // row tiles of 8 x 32 over the warps: the four 8 x 8 column tiles share each A
+  // fragment and run as four independent DMMA chains
+  for (int mt = warp; mt < P::MT; mt += P::WARPS) {
     const double* af = afrag + (size_t)mt * P::KS * 32 + lane;
-    double d0 = 0.0, d1 = 0.0;
+    double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll 5
-    for (int ks = 0; ks < P::KS; ++ks)
-      dmma_m8n8k4(d0, d1, __ldg(af + ks * 32), s_u[(ks * 4 + (lane & 3)) * LD + n0 + (lane >> 2)]);
-    *reinterpret_cast<double2*>(s_h + (mt * 8 + (lane >> 2)) * LD + n0 + 2 * (lane & 3)) = make_double2(d0, d1);
+    for (int ks = 0; ks < P::KS; ++ks) {
+      const double a = __ldg(af + ks * 32);
+      const double* bs = s_u + (ks * 4 + (lane & 3)) * LD + (lane >> 2);
+#pragma unroll
+      for (int nq = 0; nq < 4; ++nq) dmma_m8n8k4(d[nq][0], d[nq][1], a, bs[nq * 8]);
+    }
+#pragma unroll
+    for (int nq = 0; nq < 4; ++nq)
+      *reinterpret_cast<double2*>(s_h + (mt * 8 + (lane >> 2)) * LD + nq * 8 + 2 * (lane & 3)) =
+          make_double2(d[nq][0], d[nq][1]);
   }
   const bool active = lane < nel;
   const int T = T0 + (active ? lane : 0);
