@@ -165,6 +165,18 @@ def ncu_fp64_flop(nc: dict):
         return None
 
 
+def ncu_fp64_inst(nc: dict):
+    """FP64 thread instructions per launch (dfma + dmul + dadd): each occupies one
+    lane-slot of the FP64 pipe whatever its flop count, so inst/s over the
+    measured DFMA instruction rate is the pipe's utilisation."""
+    try:
+        cyc = float(nc["sm__cycles_elapsed.avg"]["value"])
+        return cyc * sum(float(nc[f"smsp__sass_thread_inst_executed_op_{k}_pred_on.sum.per_cycle_elapsed"]["value"])
+                         for k in ("dfma", "dmul", "dadd"))
+    except Exception:
+        return None
+
+
 def bench_config(m, dt, world):
     """The `config` object of both arms (identical, so the driver can match them)."""
     nb = (K_ORDER + 1) * (K_ORDER + 2)
@@ -339,6 +351,7 @@ def main():
     achieved = NT * flops / k_s / 1e12
     traffic = None     # dram read + write bytes per launch of the substep kernel (ncu --set full)
     measured_flop = None
+    measured_inst = None
     ncu_src = _latest_profile("ncu_substep_k4_r*.json")
     try:
         with open(ncu_src) as fh:
@@ -347,6 +360,7 @@ def main():
         traffic = sum(float(nc[k]["value"]) * scale[nc[k]["unit"]]
                       for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         measured_flop = ncu_fp64_flop(nc)
+        measured_inst = ncu_fp64_inst(nc)
     except Exception:
         pass
     # in-stream traffic: single-pass ncu capture of a substep batch without cache
@@ -383,6 +397,9 @@ def main():
                      # per launch) over this run's in-stream launch time
                      "hw_fp64_frac": (measured_flop / k_s / 1e12 / dfma_peak) if measured_flop else None,
                      "hw_fp64_peak_tflops": dfma_peak,
+                     # FP64 pipe slots: executed dfma + dmul + dadd thread instructions per second
+                     # over the measured DFMA instruction rate (peak TFLOP/s / 2)
+                     "hw_fp64_pipe_frac": (measured_inst / k_s / (dfma_peak * 1e12 / 2)) if measured_inst else None,
                      "hw_dram_frac": (traffic / k_s / 1e9 / hbm) if traffic else None,
                      "traffic_over_algorithmic": (traffic / (NT * byts)) if traffic else None,
                      # the same with the in-stream (warm L2, alternating sweeps) DRAM bytes per launch

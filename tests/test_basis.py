@@ -222,3 +222,27 @@ def test_dubiner_edge_trace_structure(k):
     # the traces are exact: the expansion reproduces the point values
     for e in range(3):
         assert np.allclose(L @ R[e], B.dubiner_values(k, B.ref_edge_points(e, qf.points)), atol=1e-12)
+
+
+@pytest.mark.parametrize("k", [3, 4, 5, 6, 7, 8])
+def test_mirror_symmetry_of_collapsed_and_facet_tables(k):
+    """The device kernels evaluate the Gauss-Legendre direction in mirror pairs
+    (conv2d_sf.cuh SF::SYM; sf_setup rejects tables without the symmetry):
+    A_i(n-1-a) = (-1)^i A_i(a), A'_i(n-1-a) = (-1)^(i+1) A'_i(a) on the collapsed
+    rule, and L_l(t_{nf-1-q}) = (-1)^l L_l(t_q) on the facet rule."""
+    t = B.collapsed_tables(k)
+    sg = (-1.0) ** np.arange(k + 1)
+    assert np.abs(t["A"][::-1] - sg * t["A"]).max() < 1e-13
+    assert np.abs(t["Ad"][::-1] + sg * t["Ad"]).max() < 1e-12
+    L = B.legendre_values(k, B.facet_rule(k).points)
+    assert np.abs(L[::-1] - sg * L).max() < 1e-13
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_mirror_symmetry_of_collapsed_tables_3d(k):
+    """Same for the a direction of the collapsed tet rule (conv3d.cuh HDGC_3D_SYM)."""
+    from paper_1508_04245_b200 import basis3d as B3
+    t = B3.collapsed_tables3(k)
+    sg = (-1.0) ** np.arange(k + 1)
+    assert np.abs(t["A"][::-1] - sg * t["A"]).max() < 1e-13
+    assert np.abs(t["Ad"][::-1] + sg * t["Ad"]).max() < 1e-12
