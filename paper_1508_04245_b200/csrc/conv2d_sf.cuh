@@ -398,7 +398,26 @@ struct PrepMma {
 };
 
 template <int K>
-__global__ void __launch_bounds__(32 * SF<K>::N, K == 4 ? 4 : (K <= 6 ? 3 : 2))
+#ifndef HDGC_PREP_CPASYNC
+#define HDGC_PREP_CPASYNC 0
+#endif
+// resident CTAs per SM (register caps), measured on the cfg2-size single apply:
+// k=4 4 / 5 / 6 CTAs (76 / 64 / 56 registers, no spills) 93.2 / 89.2 / 87.1 us
+#ifndef HDGC_PREP_MINB4
+#define HDGC_PREP_MINB4 6
+#endif
+// k=5 3 / 4 / 5 CTAs 185.8 / 183.3 / 184.4 us, k=6 3 / 4 / 5 CTAs 250.7 / 255.0 / 318 (spills),
+// k=7, 8 2 / 3 CTAs 541 / 554 and 785 / 820
+#ifndef HDGC_PREP_MINB5
+#define HDGC_PREP_MINB5 4
+#endif
+#ifndef HDGC_PREP_MINB56
+#define HDGC_PREP_MINB56 3
+#endif
+#ifndef HDGC_PREP_MINB78
+#define HDGC_PREP_MINB78 2
+#endif
+__global__ void __launch_bounds__(32 * SF<K>::N, K == 4 ? HDGC_PREP_MINB4 : K == 5 ? HDGC_PREP_MINB5 : (K <= 6 ? HDGC_PREP_MINB56 : HDGC_PREP_MINB78))
 prep_tile2d_kernel(const double* __restrict__ tab, const double* __restrict__ afrag, const double* __restrict__ u,
                    int nt, double* __restrict__ prep) {
   pdl_trigger();   // the update kernel after a prep may launch now (PDL, SFParams::prep_dep)
@@ -418,6 +437,18 @@ prep_tile2d_kernel(const double* __restrict__ tab, const double* __restrict__ af
     // all of this thread's u loads in flight before the first smem store (a
     // rolled load->store loop serialised the global latency: 40% of the stalls)
     constexpr int LOADS = (32 * NB + NTH - 1) / NTH;
+#if HDGC_PREP_CPASYNC
+    // straight into the transposed position with cp.async (no register round trip)
+#pragma unroll
+    for (int r = 0; r < LOADS; ++r) {
+      const int i = tid + r * NTH;
+      if (i < 32 * NB) {
+        if (i / NB < nel) cp_async8(&s_u[(i % NB) * LD + i / NB], u + (size_t)T0 * NB + i);
+        else s_u[(i % NB) * LD + i / NB] = 0.0;
+      }
+    }
+    cp_async_wait_all();
+#else
     double v[LOADS];
 #pragma unroll
     for (int r = 0; r < LOADS; ++r) {
@@ -429,6 +460,7 @@ prep_tile2d_kernel(const double* __restrict__ tab, const double* __restrict__ af
       const int i = tid + r * NTH;
       if (i < 32 * NB) s_u[(i % NB) * LD + i / NB] = v[r];
     }
+#endif
   }
   for (int i = tid; i < (P::KS * 4 - NB) * 32; i += NTH) s_u[(NB + i / 32) * LD + (i & 31)] = 0.0;
   __syncthreads();

@@ -235,8 +235,13 @@ struct Prep3Mma {
   static constexpr int SMEM = KS * 4 * LD + MT * 8 * LD;   // doubles: s_u | s_h
 };
 
+// k <= 3: three CTAs per SM (128 registers; k = 3 spills 312 B and still gains:
+// prep 547 -> 535 us at cfg5; four CTAs / 96 registers 675 us)
+#ifndef HDGC_PREP3_MINB
+#define HDGC_PREP3_MINB 3
+#endif
 template <int K>
-__global__ void __launch_bounds__(32 * Prep3Mma<K>::WARPS)
+__global__ void __launch_bounds__(32 * Prep3Mma<K>::WARPS, K <= 2 ? 4 : K == 3 ? HDGC_PREP3_MINB : 1)
 prep_tile3d_kernel(const double* __restrict__ tab, const double* __restrict__ afrag, const double* __restrict__ u,
                    const double* __restrict__ sgn, const int32_t* __restrict__ code, int nt, int ps,
                    double* __restrict__ prep) {
