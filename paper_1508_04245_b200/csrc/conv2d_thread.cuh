@@ -490,4 +490,219 @@ conv2d_thread_kernel(ElemParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Component-split update kernel (frozen-velocity batches: PREP rows present).
+// The two Cartesian components of w are advected independently by the same
+// velocity (C^V acts on w_c componentwise), so one thread per
+// (element, component): 128 threads per 64-element tile, the component is
+// warp-uniform (threads 0..63 -> c = 0, 64..127 -> c = 1).  Half the registers
+// of the one-thread-per-element kernel (w, r, neighbour row of one component;
+// the prep rows are read from a TMA-staged smem tile where they are used
+// instead of being held in 66 registers), so twice the warps are resident and
+// each carries half the dependent FMA chain.  Every output value is computed
+// with the same FMA sequence as in conv2d_thread_kernel: bitwise identical.
+#ifndef HDGC_THR_SPLIT
+#define HDGC_THR_SPLIT 1
+#endif
+#ifndef HDGC_THR_SPLIT_MINB
+#define HDGC_THR_SPLIT_MINB 8
+#endif
+template <int K>
+__host__ __device__ constexpr int split_smem_bytes() {
+  return (thread_fd_doubles<K>() + THREAD_BLOCK * Dims<K>::NB + ThreadPrep<K>::SLOTS * THREAD_BLOCK) * 8;
+}
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(2 * THREAD_BLOCK, HDGC_THR_SPLIT_MINB)
+conv2d_thread_split_kernel(ElemParams p) {
+  static_assert(K == HDGC_ORDER && K <= 2, "thread variant: k <= 2, tables per translation unit");
+  static_assert(MODE == MODE_SUBSTEP || MODE == MODE_STAGE, "split kernel: update modes of a frozen-velocity batch");
+  static_assert(THREAD_BLOCK % 32 == 0, "component must be warp-uniform");
+  using D = Dims<K>;
+  using TP = ThreadPrep<K>;
+  constexpr int NB = D::NB, NBS = D::NBS, NF = D::NF, NQV = D::NQV;
+  if (MODE == MODE_STAGE && stage_stopped(p.st)) return;   // converged Richardson iteration
+  const double* vw = c_th + D::OFF_VW;
+  const double* vD = c_th + D::OFF_VD;
+  const double* vG = c_th + D::OFF_VG;
+  const double* fD = c_th + D::OFF_FD;
+  extern __shared__ __align__(16) double s_fD[];
+  hdgc_debug_prologue(s_fD, split_smem_bytes<K>() / 8);
+  const int el = threadIdx.x & (THREAD_BLOCK - 1);
+  const int c = threadIdx.x / THREAD_BLOCK;
+  const int tb = blockIdx.x * THREAD_BLOCK;
+  const bool active = tb + el < p.nt;
+  const int T = active ? tb + el : p.nt - 1;   // tail lanes recompute the last element, write nothing
+  const int nel = min(THREAD_BLOCK, p.nt - tb);
+  double* s_w = s_fD + thread_fd_doubles<K>();
+  double* s_p = s_w + THREAD_BLOCK * NB;
+  __shared__ __align__(8) uint64_t tbar[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&tbar[0], 1);
+    mbar_init(&tbar[1], 1);
+    fence_mbar_init();
+    // the tile's frozen-velocity rows [slot][64]: written by prep_thread2d_kernel
+    // before this batch (never launched with a PDL edge to it), so requested
+    // first thing, before the table fill and the wait
+    constexpr uint32_t pbytes = TP::SLOTS * THREAD_BLOCK * sizeof(double);
+    mbar_arrive_expect_tx(&tbar[0], pbytes);
+    bulk_g2s(s_p, p.prep + (size_t)blockIdx.x * TP::SLOTS * THREAD_BLOCK, pbytes, &tbar[0]);
+  }
+  for (int i = threadIdx.x; i < 3 * NF * NBS; i += blockDim.x) s_fD[i] = p.tab[D::OFF_FD + i];
+  int code[3];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) code[e] = __ldg(p.code + (size_t)T * 3 + e);
+  const double mi = __ldg(p.minv + T);
+  __syncthreads();   // mbarrier init visible, s_fD complete
+  // w (and x) are the previous update kernel's output under a PDL launch
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&tbar[1], (uint32_t)(nel * NB * sizeof(double)));
+    bulk_g2s(s_w, p.w + (size_t)tb * NB, (uint32_t)(nel * NB * sizeof(double)), &tbar[1]);
+  }
+  double xs[MODE == MODE_STAGE ? NBS : 1];
+  if constexpr (MODE == MODE_STAGE) {
+    const double* xg = p.st.x + (size_t)T * NB + c * NBS;
+#pragma unroll
+    for (int j = 0; j < NBS; ++j) xs[j] = __ldg(xg + j);
+  }
+  mbar_wait(&tbar[1], 0);
+  double w[NBS];
+  {
+    const double* ws = s_w + (T - tb) * NB + c * NBS;
+#pragma unroll
+    for (int j = 0; j < NBS; ++j) w[j] = ws[j];
+  }
+  mbar_wait(&tbar[0], 0);
+  const double* pr = s_p + el;
+  double r[NBS];
+#pragma unroll
+  for (int j = 0; j < NBS; ++j) r[j] = 0.0;
+
+  // ---- volume: f_c = u.grad w_c + w_c div u, tested against D_m
+#pragma unroll
+  for (int q = 0; q < NQV; ++q) {
+    const double* Dq = vD + q * NBS;
+    const double* Gq = vG + q * NBS * 2;
+    double w0 = 0.0, wx = 0.0, wy = 0.0;
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) {
+      w0 = fma(w[m], Dq[m], w0);
+      wx = fma(w[m], Gq[2 * m], wx);
+      wy = fma(w[m], Gq[2 * m + 1], wy);
+    }
+    const double u0 = pr[(3 * q) * THREAD_BLOCK], u1 = pr[(3 * q + 1) * THREAD_BLOCK];
+    const double dvq = pr[(3 * q + 2) * THREAD_BLOCK];
+    const double f = vw[q] * fma(u0, wx, fma(u1, wy, w0 * dvq));
+#pragma unroll
+    for (int m = 0; m < NBS; ++m) r[m] = fma(f, Dq[m], r[m]);
+  }
+
+  // ---- facets: upwind jump on inflow points only (element-owned, no atomics).
+  // (Measured and not adopted: neighbour rows requested one edge ahead through a
+  // generic smem-or-global pointer, 53.7 -> 63-72 us at 524k triangles.)
+#pragma unroll
+  for (int e = 0; e < 3; ++e) {
+    double F[NF];   // inflow weights s_q = w_q F_e(t_q) where F < 0, else 0
+    bool inflow_edge = false;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      F[q] = pr[(TP::S_FAC + e * NF + q) * THREAD_BLOCK];
+      inflow_edge |= F[q] != 0.0;
+    }
+    if (!inflow_edge) continue;  // pure outflow edge: w_hat = own trace, jump = 0
+    const int cd = code[e];
+    const double* infl = nullptr;
+    double wn[NBS];
+    int e2 = 0;
+    if (cd >= 0) {
+      HDGC_ASSERT((cd >> 2) < p.nt && (cd & 3) < 3);
+      const int nbT = cd >> 2;
+      e2 = cd & 3;
+      if (nbT >= tb && nbT < tb + nel) {
+        const double* ws = s_w + (nbT - tb) * NB + c * NBS;   // in-tile neighbour: its row is staged
+#pragma unroll
+        for (int j = 0; j < NBS; ++j) wn[j] = ws[j];
+      } else {
+        const double* wg = p.w + (size_t)nbT * NB + c * NBS;
+#pragma unroll
+        for (int j = 0; j < NBS; ++j) wn[j] = __ldg(wg + j);
+      }
+    } else if (p.inflow != nullptr) {
+      infl = p.inflow + (size_t)(-1 - cd) * NF * 2 + c;
+    } else {
+      continue;  // boundary without inflow data: exterior value = own trace
+    }
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      const double Fq = F[q];
+      if (Fq == 0.0) continue;
+      const double* De = fD + (e * NF + q) * NBS;
+      double o = 0.0;
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) o = fma(w[m], De[m], o);
+      double x;
+      if (cd >= 0) {
+        const double* Dn = s_fD + (e2 * NF + (NF - 1 - q)) * NBS;
+        x = 0.0;
+#pragma unroll
+        for (int m = 0; m < NBS; ++m) x = fma(wn[m], Dn[m], x);
+      } else {
+        x = __ldg(infl + 2 * q);
+      }
+      const double jmp = Fq * (x - o);
+#pragma unroll
+      for (int m = 0; m < NBS; ++m) r[m] = fma(jmp, De[m], r[m]);
+    }
+  }
+
+  // ---- epilogue
+  if (p.st.cres && active && mi < 0.0) {
+    // curved element: hand the raw residual to curved_fixup_kernel
+    double* cr = p.st.cres + (size_t)((int)(-mi) - 1) * NB + c * NBS;
+#pragma unroll
+    for (int j = 0; j < NBS; ++j) cr[j] = r[j];
+  }
+  const double cm = p.st.c * mi;
+  if constexpr (MODE == MODE_SUBSTEP) {
+    // the rows go back through the w tile and one bulk store (coalesced)
+    double v[NBS];
+    double chk = 0.0;
+#pragma unroll
+    for (int j = 0; j < NBS; ++j) {
+      v[j] = fma(cm, r[j], w[j]);
+      chk += v[j];
+    }
+    guard_finite(p.st.flag, chk);
+    __syncthreads();   // every thread's facet loop is done reading the w tile
+    if (active) {
+      double* ws = s_w + (T - tb) * NB + c * NBS;
+#pragma unroll
+      for (int j = 0; j < NBS; ++j) ws[j] = v[j];
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_s2g(p.out + (size_t)tb * NB, s_w, (uint32_t)(nel * NB * sizeof(double)));
+      bulk_wait_read();
+    }
+  } else {
+    if (!active) return;
+    double* og = p.out + (size_t)T * NB + c * NBS;
+    const double tm = -p.st.tau * mi;
+    double acc = 0.0, chk = 0.0;
+#pragma unroll
+    for (int j = 0; j < NBS; ++j) {
+      const double v = fma(p.st.b, xs[j], fma(cm, r[j], p.st.a * w[j]));
+      og[j] = v;
+      chk += v;
+      const double res = fma(tm, r[j], xs[j] - w[j]);
+      acc = fma(res, res, acc);
+    }
+    guard_finite(p.st.flag, chk);
+    if (p.st.rn) p.st.rn[2 * (size_t)T + c] = acc;
+  }
+}
+
 }  // namespace hdgc

@@ -115,6 +115,25 @@ int launch_elem(hdgc_ctx* c, int mode, const double* u, const double* w, const d
   };
   if (c->tprep_on && c->d_tprep) {
     p.prep = c->d_tprep;
+#if HDGC_THR_SPLIT
+    // one thread per (element, component): 128 threads per 64-element tile
+    auto launch2 = [&](auto kern) -> int {
+      constexpr int smem2 = split_smem_bytes<K>();
+      if (smem2 > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+      CUDA_TRY(launch_maybe_pdl(kern, blocks, 2 * threads, smem2, st, c->pdl, p));
+      return HDGC_OK;
+    };
+    // measured (profiles/split_k2_r02.jsonl): ahead once w, out and the prep rows no
+    // longer fit the L2 together (k=2, 524k triangles: 59.2 -> 53.7 us, 4.6 TB/s of
+    // DRAM), behind while they do (131k: 15.5 vs 14.3-15.0 us; k=1: 7.7 vs 6.4 us)
+    // HDGC_SPLIT=1 / 0 forces it on / off (tests run both kernels on small meshes)
+    static const int split_force = [] { const char* se = getenv("HDGC_SPLIT"); return se ? (se[0] == '0' ? -1 : 1) : 0; }();
+    const bool split = K == 2 && (split_force > 0 ||
+                                  (split_force == 0 &&
+                                   (size_t)c->nt * (ThreadPrep<K>::SLOTS + 2 * Dims<K>::NB) * 8 > ((size_t)96 << 20)));
+    if (split && mode == MODE_SUBSTEP) return launch2(conv2d_thread_split_kernel<K, MODE_SUBSTEP>);
+    if (split && mode == MODE_STAGE) return launch2(conv2d_thread_split_kernel<K, MODE_STAGE>);
+#endif
     if (mode == MODE_SUBSTEP) return launch(conv2d_thread_kernel<K, MODE_SUBSTEP, true>);
     if (mode == MODE_STAGE) return launch(conv2d_thread_kernel<K, MODE_STAGE, true>);
   }

@@ -309,3 +309,60 @@ def test_shuffled_element_order_halo_paths(k):
     dt = F.cfl_dt(m.h_min(), k, F.max_speed_host(m, k, u))
     wd = op.substeps(dev(u), dev(w), dt, 6, dev(inflow))
     assert rel(wd, port.substeps(u, w, dt, 6, inflow)) < SUBSTEP_TOL
+
+
+_SPLIT_SCRIPT = r"""
+import sys, hashlib, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from oracle import port as P
+from paper_1508_04245_b200 import fields as F, mesh as M, timeloop as TL
+from paper_1508_04245_b200.forms import ConvectionOperator
+dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+k = 2
+h = hashlib.sha256()
+errs = []
+for (nx, ny) in ((7, 5), (96, 96)):   # ragged tail tile; many CTA waves
+    m = M.generate_structured((0.0, 0.0, 1.3, 0.7), nx, ny)
+    sf = F.StreamFunction(5, 4, (0.8, -0.5))
+    u = F.interpolate_curl(m, k, sf)
+    w = F.transfer_I_host(m, k, u)
+    inflow = F.inflow_values(m, k, sf)
+    op = ConvectionOperator(m, k)
+    dt = F.cfl_dt(m.h_min(), k, F.max_speed_host(m, k, u))
+    ud, infd = dev(u), dev(inflow)
+    batch = op.substeps(ud, dev(w), dt, 12, infd)          # prep + 12 update kernels (PDL)
+    assert torch.equal(batch, op.substeps(ud, dev(w), dt, 12, infd))
+    ref = P.PortOperator(m, k, threads=2).substeps(u, w, dt, 12, inflow)
+    errs.append(float(np.linalg.norm(batch.cpu().numpy() - ref) / np.linalg.norm(ref)))
+    h.update(batch.cpu().numpy().tobytes())
+    a = dev(w)
+    op.propagate(ud, a, 0.5 * dt, 6, infd, "ssprk2")      # SUBSTEP + STAGE kernels
+    h.update(a.cpu().numpy().tobytes())
+    g = dev(np.random.default_rng(3).standard_normal(w.shape))
+    v, it, conv, r0, rn = op.richardson(ud, g, torch.zeros_like(g), 3 * dt, dt, 1e-6, 300, infd)
+    h.update(v.cpu().numpy().tobytes()); h.update(np.float64([it, r0, rn]).tobytes())
+    op.check_finite()
+print(h.hexdigest(), " ".join(f"{x:.3e}" for x in errs))
+"""
+
+
+def test_component_split_kernel_bitwise_equals_thread_kernel():
+    """k = 2 frozen-velocity batches on large meshes run the component-split
+    update kernel (one thread per (element, component), conv2d_thread.cuh);
+    HDGC_SPLIT=1 / 0 force it on / off.  Substep batches (ragged tail tile and a
+    many-wave mesh, inflow data), SSP-RK2 propagation (STAGE mode) and a
+    Richardson solve must be bitwise identical between the two kernels, and the
+    split batch within the substep tolerance of the C port."""
+    import os
+    import subprocess
+    import sys
+    tests = os.path.dirname(os.path.abspath(__file__))
+    outs = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, HDGC_SPLIT=flag)
+        res = subprocess.run([sys.executable, "-c", _SPLIT_SCRIPT, tests], env=env, capture_output=True, text=True,
+                             timeout=600, cwd=os.path.dirname(tests))
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(res.stdout.split())
+    assert outs[0][0] == outs[1][0], outs
+    assert max(float(x) for x in outs[0][1:]) < SUBSTEP_TOL, outs
