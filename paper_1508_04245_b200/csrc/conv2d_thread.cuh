@@ -49,6 +49,24 @@ __host__ __device__ constexpr int thread_smem_bytes() {
   return (thread_fd_doubles<K>() + (HDGC_THR_TMA ? 2 * THREAD_BLOCK * Dims<K>::NB : 0)) * 8;
 }
 
+// copy a row of N doubles (16-byte aligned when N is even) with 16-byte
+// accesses where possible
+template <int N, bool LDG = false>
+__device__ __forceinline__ void row_load(double* dst, const double* src) {
+  if constexpr (N % 2 == 0) {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+#pragma unroll
+    for (int j = 0; j < N / 2; ++j) {
+      const double2 t = LDG ? __ldg(s2 + j) : s2[j];
+      dst[2 * j] = t.x;
+      dst[2 * j + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) dst[j] = LDG ? __ldg(src + j) : src[j];
+  }
+}
+
 // Frozen-velocity prep of the thread variant (substep batches, hdgc_propagate,
 // Richardson: u is frozen over the batch): per element the
 // velocity at the NQV volume points, u_hat_0(q), u_hat_1(q), div u_hat(q), and
@@ -336,13 +354,9 @@ conv2d_thread_kernel(ElemParams p) {
       const int nbT = code >> 2;
       e2 = code & 3;
       if (HDGC_THR_TMA && nbT >= tb && nbT < tb + nel) {
-        const double* ws = s_w + (nbT - tb) * NB;   // in-tile neighbour: its row is staged
-#pragma unroll
-        for (int j = 0; j < NB; ++j) wn[j] = ws[j];
+        row_load<NB>(wn, s_w + (nbT - tb) * NB);   // in-tile neighbour: its row is staged
       } else {
-        const double* wg = p.w + (size_t)nbT * NB;
-#pragma unroll
-        for (int j = 0; j < NB; ++j) wn[j] = __ldg(wg + j);
+        row_load<NB, true>(wn, p.w + (size_t)nbT * NB);
       }
     } else if (p.inflow != nullptr) {
       infl = p.inflow + (size_t)(-1 - code) * NF * 2;
@@ -362,7 +376,8 @@ conv2d_thread_kernel(ElemParams p) {
       }
       double x0, x1;
       if (code >= 0) {
-        const double* Dn = s_fD + (e2 * NF + (NF - 1 - q)) * NBS;
+        double Dn[NBS];   // per-lane row (the neighbour's local edge): 16-byte LDS when NBS is even
+        row_load<NBS>(Dn, s_fD + (e2 * NF + (NF - 1 - q)) * NBS);
         x0 = 0.0; x1 = 0.0;
 #pragma unroll
         for (int m = 0; m < NBS; ++m) {
@@ -570,9 +585,7 @@ conv2d_thread_split_kernel(ElemParams p) {
   mbar_wait(&tbar[1], 0);
   double w[NBS];
   {
-    const double* ws = s_w + (T - tb) * NB + c * NBS;
-#pragma unroll
-    for (int j = 0; j < NBS; ++j) w[j] = ws[j];
+    row_load<NBS>(w, s_w + (T - tb) * NB + c * NBS);
   }
   mbar_wait(&tbar[0], 0);
   const double* pr = s_p + el;
@@ -621,13 +634,9 @@ conv2d_thread_split_kernel(ElemParams p) {
       const int nbT = cd >> 2;
       e2 = cd & 3;
       if (nbT >= tb && nbT < tb + nel) {
-        const double* ws = s_w + (nbT - tb) * NB + c * NBS;   // in-tile neighbour: its row is staged
-#pragma unroll
-        for (int j = 0; j < NBS; ++j) wn[j] = ws[j];
+        row_load<NBS>(wn, s_w + (nbT - tb) * NB + c * NBS);   // in-tile neighbour: its row is staged
       } else {
-        const double* wg = p.w + (size_t)nbT * NB + c * NBS;
-#pragma unroll
-        for (int j = 0; j < NBS; ++j) wn[j] = __ldg(wg + j);
+        row_load<NBS, true>(wn, p.w + (size_t)nbT * NB + c * NBS);
       }
     } else if (p.inflow != nullptr) {
       infl = p.inflow + (size_t)(-1 - cd) * NF * 2 + c;
@@ -644,7 +653,8 @@ conv2d_thread_split_kernel(ElemParams p) {
       for (int m = 0; m < NBS; ++m) o = fma(w[m], De[m], o);
       double x;
       if (cd >= 0) {
-        const double* Dn = s_fD + (e2 * NF + (NF - 1 - q)) * NBS;
+        double Dn[NBS];   // per-lane row (the neighbour's local edge): 16-byte LDS
+        row_load<NBS>(Dn, s_fD + (e2 * NF + (NF - 1 - q)) * NBS);
         x = 0.0;
 #pragma unroll
         for (int m = 0; m < NBS; ++m) x = fma(wn[m], Dn[m], x);
@@ -678,8 +688,13 @@ conv2d_thread_split_kernel(ElemParams p) {
     __syncthreads();   // every thread's facet loop is done reading the w tile
     if (active) {
       double* ws = s_w + (T - tb) * NB + c * NBS;
+      if constexpr (NBS % 2 == 0) {
 #pragma unroll
-      for (int j = 0; j < NBS; ++j) ws[j] = v[j];
+        for (int j = 0; j < NBS / 2; ++j) reinterpret_cast<double2*>(ws)[j] = make_double2(v[2 * j], v[2 * j + 1]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < NBS; ++j) ws[j] = v[j];
+      }
     }
     fence_proxy_async();
     __syncthreads();
