@@ -12,6 +12,8 @@ changes the result; an out-of-range index traps.  Every case also runs twice
 per library (run-to-run determinism).
 
   python tools/debug_check.py            # both libraries, prints a JSON summary
+  python tools/debug_check.py split      # the same for the k = 2 component-split kernel
+                                         # (HDGC_SPLIT=1; ragged and many-wave meshes)
   python tools/debug_check.py run OUT.npz  # (internal) one library, HDGC_LIB selects it
 """
 import json
@@ -36,6 +38,29 @@ def run(out):
 
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()   # noqa: E731
     res = {}
+    if os.environ.get("HDGC_SPLIT") == "1":   # split mode: k = 2 frozen-velocity batches only
+        for nx, ny in ((7, 5), (24, 24), (96, 96)):
+            m = M.generate_structured((0, 0, 1.3, 0.7), nx, ny)
+            sf = F.StreamFunction(4, 1, (1.0, 0.3))
+            u = F.interpolate_curl(m, 2, sf)
+            w = F.transfer_I_host(m, 2, u)
+            inf = F.inflow_values(m, 2, sf)
+            op = ConvectionOperator(m, 2)
+            ud, wd, infd = dev(u), dev(w), dev(inf)
+            dt = F.cfl_dt(m.h_min(), 2, F.max_speed_host(m, 2, u))
+            for rep in range(2):
+                tag = f"split{nx}x{ny}"
+                res[f"{tag}_sub_{rep}"] = op.substeps(ud, wd.clone(), dt, 12, infd).cpu().numpy()
+                a = wd.clone()
+                op.propagate(ud, a, 0.5 * dt, 6, infd, "ssprk2")
+                res[f"{tag}_rk2_{rep}"] = a.cpu().numpy()
+                v, it, conv, _, _ = op.richardson(ud, wd, torch.zeros_like(wd), 5 * dt, 0.3, 1e-4, 40, infd)
+                res[f"{tag}_rich_{rep}"] = v.cpu().numpy()
+                res[f"{tag}_richit_{rep}"] = np.array([it])
+            op.check_finite()
+        torch.cuda.synchronize()
+        np.savez(out, **res)
+        return
     for k in range(1, 9):
         for modal in ([False, True] if 4 <= k <= 6 else [False]):
             os.environ["HDGC_MODAL"] = str(k) if modal else "0"
@@ -80,6 +105,9 @@ def main():
         return
     env = dict(os.environ)
     env.pop("HDGC_LIB", None)
+    env.pop("HDGC_SPLIT", None)
+    if len(sys.argv) > 1 and sys.argv[1] == "split":
+        env["HDGC_SPLIT"] = "1"
     subprocess.check_call([sys.executable, __file__, "run", "/tmp/dbg_release.npz"], env=env)
     env["HDGC_LIB"] = DEBUG_LIB
     rc = subprocess.call([sys.executable, __file__, "run", "/tmp/dbg_debug.npz"], env=env)

@@ -16,7 +16,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OPS = ["DMMA", "DFMA", "DMUL", "DADD", "UBLKCP", "UTMALDG", "UTMASTG", "SYNCS", "LDGSTS", "LDL", "STL", "LDS",
        "STS", "LDC", "LDG", "STG", "SHFL", "BAR"]
-INTERESTING = re.compile(r"conv2d_sf_kernel|conv2d_sfm_kernel|conv2d_thread_kernel|conv3d_kernel|prep_tile2d|"
+INTERESTING = re.compile(r"conv2d_sf_kernel|conv2d_sfm_kernel|conv2d_thread_kernel|conv2d_thread_split_kernel|prep_thread2d|conv3d_kernel|prep_tile2d|"
                          r"prep_modal2d|prep_tile3d|prep_fused2d|richardson|modal_rows")
 
 
