@@ -722,8 +722,18 @@ conv3d_kernel(Conv3Params p) {
       if (code >= 0) {
         const double* g = p.w + (size_t)(code >> 2) * NB + c * NBS;
         f2 = code & 3;
+        if constexpr (NBS % 2 == 0) {   // component rows are 16-byte aligned: half as many loads
+          const double2* g2 = reinterpret_cast<const double2*>(g);
 #pragma unroll
-        for (int m = 0; m < NBS; ++m) s_wn[m * 96 + threadIdx.x] = __ldg(g + m);
+          for (int m = 0; m < NBS / 2; ++m) {
+            const double2 t = __ldg(g2 + m);
+            s_wn[(2 * m) * 96 + threadIdx.x] = t.x;
+            s_wn[(2 * m + 1) * 96 + threadIdx.x] = t.y;
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < NBS; ++m) s_wn[m * 96 + threadIdx.x] = __ldg(g + m);
+        }
       } else {
 #pragma unroll
         for (int m = 0; m < NBS; ++m) s_wn[m * 96 + threadIdx.x] = 0.0;
