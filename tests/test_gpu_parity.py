@@ -366,3 +366,20 @@ def test_component_split_kernel_bitwise_equals_thread_kernel():
         outs.append(res.stdout.split())
     assert outs[0][0] == outs[1][0], outs
     assert max(float(x) for x in outs[0][1:]) < SUBSTEP_TOL, outs
+
+
+def test_component_split_kernel_curved_and_oracle_cases():
+    """The k = 2 curved-element batches (raw residual rows handed to the curved
+    fix-up kernel, no PDL) and the Richardson-vs-oracle case again with the
+    component-split kernel forced on (HDGC_SPLIT=1, read once per process)."""
+    import os
+    import subprocess
+    import sys
+    tests = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, HDGC_SPLIT="1")
+    nodes = ["tests/test_gpu_curved.py::test_apply_substeps_transfer[2]",
+             "tests/test_gpu_curved.py::test_propagate_and_richardson[2]",
+             "tests/test_gpu_timeloop.py::test_richardson_vs_oracle[2]"]
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider", *nodes],
+                         env=env, capture_output=True, text=True, timeout=900, cwd=os.path.dirname(tests))
+    assert res.returncode == 0 and "3 passed" in res.stdout, res.stdout[-2000:] + res.stderr[-1000:]
